@@ -1,0 +1,477 @@
+/*
+ * oracle.c — plain, slow, single-threaded CPU oracle (TEST INFRASTRUCTURE ONLY).
+ *
+ * Follows Forster, arXiv 1805.10904 (/root/reference/PAPER.md, cited "P:Lnn") step by
+ * step, with the readings D1..D27 of DESIGN.md §3 wherever the paper is silent, garbled
+ * or inconsistent.  No blocking, fusion or reordering: each function is the paper's
+ * definition or algorithm written out.  Library primitives used as steps: qsort.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline, --impl reference)
+ * may load this file's library.  It shares nothing with paper_1805_10904_b200/.
+ *
+ * Parity pins: see tests/test_oracle_*.py (Eq. 3 brute force + networkx, gain
+ * consistency vs Eq. 3 differences, exhaustive optimum bound, ring of cliques,
+ * karate band, SPEC examples, Theorem 1 invariant, weight conservation).
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC.
+ */
+#include "oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __int128 i128;
+
+/* ---------------------------------------------------------------- utilities */
+
+/* D22 (as refined in DESIGN.md §3): pinned int128 → fp64 conversion on the magnitude,
+ * d(x) = sign(x) · fl(fl(hi)·2^64 + fl(lo)) with (hi,lo) the 64-bit words of |x|.
+ * (A two's-complement split fl(hi)·2^64 + fl(lo) cancels catastrophically for small
+ * negative x, e.g. d(−2) = 0; tests/test_oracle_pins.py::test_modularity_closed_forms.) */
+static double d128(i128 x) {
+    int neg = x < 0;
+    unsigned __int128 m = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
+    uint64_t hi = (uint64_t)(m >> 64), lo = (uint64_t)m;
+    double d = (double)hi * 18446744073709551616.0 + (double)lo;
+    return neg ? -d : d;
+}
+
+void og_config_default(og_config *c) {
+    c->theta = 1e-6;          /* D16 */
+    c->big_theta = 1e-6;      /* D16 */
+    c->max_sweeps = 100;      /* D12 */
+    c->max_levels = 64;       /* D27 */
+    c->stop_rule = 0;         /* D10: Alg. 1 literal */
+    c->merge_isolated = 1;    /* D14 */
+    c->theta_schedule = NULL; /* D21 */
+    c->theta_schedule_len = 0;
+}
+
+/* ------------------------------------------------------- graph construction */
+
+typedef struct { int32_t u, v; int64_t w; } rec_t;
+
+static int rec_cmp(const void *a, const void *b) {
+    const rec_t *x = (const rec_t *)a, *y = (const rec_t *)b;
+    if (x->u != y->u) return x->u < y->u ? -1 : 1;
+    if (x->v != y->v) return x->v < y->v ? -1 : 1;
+    return 0;
+}
+
+static og_graph *graph_alloc(int64_t n, int64_t nnz) {
+    og_graph *g = (og_graph *)calloc(1, sizeof(og_graph));
+    if (!g) return NULL;
+    g->n = n;
+    g->nnz = nnz;
+    g->row_ptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    g->col = (int32_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
+    g->w = (int64_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int64_t));
+    g->loop = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    g->delta = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    if (!g->row_ptr || !g->col || !g->w || !g->loop || !g->delta) { og_graph_free(g); return NULL; }
+    return g;
+}
+
+void og_graph_free(og_graph *g) {
+    if (!g) return;
+    free(g->row_ptr); free(g->col); free(g->w); free(g->loop); free(g->delta);
+    free(g);
+}
+
+/* Build CSR from sorted, merged directed records (u,v,w); loops already in g->loop. */
+static void fill_csr(og_graph *g, rec_t *r, int64_t cnt) {
+    int64_t out = 0;
+    for (int64_t k = 0; k < cnt; ++k) {           /* merge duplicates by summing (D25) */
+        if (out > 0 && r[out - 1].u == r[k].u && r[out - 1].v == r[k].v) r[out - 1].w += r[k].w;
+        else r[out++] = r[k];
+    }
+    g->nnz = out;
+    for (int64_t k = 0; k < out; ++k) g->row_ptr[r[k].u + 1]++;
+    for (int64_t i = 0; i < g->n; ++i) g->row_ptr[i + 1] += g->row_ptr[i];   /* exclusive scan */
+    for (int64_t k = 0; k < out; ++k) { g->col[k] = r[k].v; g->w[k] = r[k].w; }
+    /* δ_i = Σ_{j∈Γ(i)} ω(i,j) with a loop counted twice (D2) */
+    for (int64_t i = 0; i < g->n; ++i) {
+        int64_t s = 2 * g->loop[i];
+        for (int64_t e = g->row_ptr[i]; e < g->row_ptr[i + 1]; ++e) s += g->w[e];
+        g->delta[i] = s;
+    }
+}
+
+/* §5.1.2 "Neighbor computation": mirror every non-loop record, sort by
+ * (source,target), merge, offsets by exclusive scan.  Loops go to loop[] (D2). */
+int og_graph_build(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                   const int64_t *w, og_graph **out) {
+    *out = NULL;
+    if (n <= 0 || m < 0) return OG_EINVAL;
+    rec_t *r = (rec_t *)malloc((size_t)(2 * m > 0 ? 2 * m : 1) * sizeof(rec_t));
+    og_graph *g = graph_alloc(n, 0);
+    if (!r || !g) { free(r); og_graph_free(g); return OG_ENOMEM; }
+    int64_t cnt = 0, W = 0;
+    for (int64_t k = 0; k < m; ++k) {
+        int32_t u = src[k], v = dst[k];
+        int64_t wk = w ? w[k] : 1;                 /* D1: unweighted ⇒ 1 */
+        if (u < 0 || v < 0 || u >= n || v >= n || wk <= 0) { free(r); og_graph_free(g); return OG_EGRAPH; }
+        W += wk;                                    /* D3: W = Σ weights, loops once */
+        if (u == v) { g->loop[u] += wk; continue; }
+        r[cnt].u = u; r[cnt].v = v; r[cnt].w = wk; ++cnt;
+        r[cnt].u = v; r[cnt].v = u; r[cnt].w = wk; ++cnt;
+    }
+    qsort(r, (size_t)cnt, sizeof(rec_t), rec_cmp);
+    free(g->col); free(g->w);
+    g->col = (int32_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int32_t));
+    g->w = (int64_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int64_t));
+    if (!g->col || !g->w) { free(r); og_graph_free(g); return OG_ENOMEM; }
+    fill_csr(g, r, cnt);
+    free(r);
+    g->W = W;
+    *out = g;
+    return W > 0 ? OG_OK : OG_EZEROW;
+}
+
+/* ----------------------------------------------------------- community state */
+
+struct og_state {
+    const og_graph *g;
+    const int32_t *C;    /* snapshot labels (borrowed)                 */
+    int64_t *deg;        /* deg_C (Eq. 2), indexed by label            */
+    int64_t *size;       /* |C|, indexed by label                      */
+    int64_t *e;          /* scratch: e_{i→c} accumulator (Eq. 1)       */
+    uint8_t *mark;       /* scratch: c touched                         */
+    int32_t *touched;    /* scratch: list of touched labels            */
+};
+
+og_state *og_state_new(const og_graph *g, const int32_t *labels) {
+    og_state *st = (og_state *)calloc(1, sizeof(og_state));
+    if (!st) return NULL;
+    int64_t n = g->n;
+    st->g = g;
+    st->C = labels;
+    st->deg = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    st->size = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    st->e = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    st->mark = (uint8_t *)calloc((size_t)n, 1);
+    st->touched = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!st->deg || !st->size || !st->e || !st->mark || !st->touched) { og_state_free(st); return NULL; }
+    for (int64_t i = 0; i < n; ++i) {            /* Eq. 2: deg_C = Σ_{i∈C} δ_i */
+        st->deg[labels[i]] += g->delta[i];
+        st->size[labels[i]] += 1;
+    }
+    return st;
+}
+
+void og_state_free(og_state *st) {
+    if (!st) return;
+    free(st->deg); free(st->size); free(st->e); free(st->mark); free(st->touched);
+    free(st);
+}
+
+/* The decision of vertex i against the snapshot (Algorithm 1 body).
+ *  mode 0 (local move):
+ *   N_i = {C(i)} ∪ {C(j) : j ∈ Γ(i)}, loops excluded (D5)
+ *   e_{i→c} per Eq. 1; gain of moving to c relative to staying, Eq. 4 read as D4:
+ *     S(c)   = 2W·e_{i→c} − δ_i·deg_c                   (c ≠ C(i))
+ *     S_own  = 2W·e_{i→C(i)} − δ_i·(deg_{C(i)} − δ_i)   (C(i)\{i})
+ *     ΔQ_{i→c} = (S(c) − S_own) / (2W²)
+ *   target = argmax ΔQ, ties → minimum label (Eq. 5, §3.1.2; D7)
+ *   move iff ΔQ_{i→target} > 0 (D6 strict)
+ *   singlet rule: singlet → singlet only if l(target) < l(C(i)) (§3.1.1; D8: else stay)
+ *  mode 1 (isolated merge; D14): a singlet whose neighbours lie in exactly one
+ *   community T moves to T (singlet rule applies). */
+int32_t og_decide(const og_state *st, int64_t i, int32_t mode) {
+    const og_graph *g = st->g;
+    const int32_t *C = st->C;
+    int32_t own = C[i];
+    int64_t b = g->row_ptr[i], eend = g->row_ptr[i + 1];
+    if (b == eend) return own;                       /* no non-loop neighbours */
+    if (mode == 1 && st->size[own] != 1) return own; /* D14: singlets only     */
+    int64_t nt = 0;
+    for (int64_t k = b; k < eend; ++k) {             /* Eq. 1 */
+        int32_t c = C[g->col[k]];
+        if (!st->mark[c]) { st->mark[c] = 1; st->touched[nt++] = c; }
+        st->e[c] += g->w[k];
+    }
+    int32_t result = own;
+    if (mode == 0) {
+        i128 twoW = (i128)2 * g->W;
+        i128 di = g->delta[i];
+        int64_t e_own = st->mark[own] ? st->e[own] : 0;
+        i128 S_own = twoW * e_own - di * ((i128)st->deg[own] - di);
+        int32_t best = -1;
+        i128 S_best = 0;
+        for (int64_t t = 0; t < nt; ++t) {
+            int32_t c = st->touched[t];
+            if (c == own) continue;
+            i128 S = twoW * st->e[c] - di * (i128)st->deg[c];
+            if (best < 0 || S > S_best || (S == S_best && c < best)) { best = c; S_best = S; }
+        }
+        if (best >= 0 && S_best > S_own) {
+            if (st->size[own] == 1 && st->size[best] == 1 && best > own) result = own;
+            else result = best;
+        }
+    } else {
+        int32_t T = -1;
+        int64_t distinct = 0;
+        for (int64_t t = 0; t < nt; ++t)
+            if (st->touched[t] != own) { ++distinct; T = st->touched[t]; }
+        if (distinct == 1) {
+            if (st->size[T] == 1 && T > own) result = own;
+            else result = T;
+        }
+    }
+    for (int64_t t = 0; t < nt; ++t) { st->e[st->touched[t]] = 0; st->mark[st->touched[t]] = 0; }
+    return result;
+}
+
+int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_out, int32_t mode) {
+    og_state *st = og_state_new(g, labels_in);
+    if (!st) return -1;
+    int64_t moved = 0;
+    for (int64_t i = 0; i < g->n; ++i) {   /* Jacobi: every decision reads the snapshot (D9) */
+        labels_out[i] = og_decide(st, i, mode);
+        moved += labels_out[i] != labels_in[i];
+    }
+    og_state_free(st);
+    return moved;
+}
+
+/* ---------------------------------------------------------------- modularity */
+
+/* Eq. 3: Q = (1/2W) Σ_i e_{i→C(i)} − Σ_C (deg_C/2W)², with e_{i→C(i)} counting a loop
+ * twice (D2, D24).  Exact numerator 2W·I2 − S2 over 4W². */
+static void modularity_num(const og_graph *g, const int32_t *C, const int64_t *deg,
+                           int64_t *I2, i128 *S2) {
+    int64_t s = 0;
+    for (int64_t i = 0; i < g->n; ++i) {
+        s += 2 * g->loop[i];
+        for (int64_t k = g->row_ptr[i]; k < g->row_ptr[i + 1]; ++k)
+            if (C[g->col[k]] == C[i]) s += g->w[k];
+    }
+    i128 q = 0;
+    for (int64_t c = 0; c < g->n; ++c) q += (i128)deg[c] * deg[c];
+    *I2 = s;
+    *S2 = q;
+}
+
+static double q_from_num(int64_t W, int64_t I2, i128 S2) {
+    i128 num = (i128)2 * W * I2 - S2;
+    i128 den = (i128)4 * W * W;
+    return d128(num) / d128(den);
+}
+
+int og_modularity(const og_graph *g, const int32_t *labels, int64_t *I2,
+                  int64_t *S2_hi, uint64_t *S2_lo, double *Q) {
+    if (g->W <= 0) return OG_EZEROW;
+    int64_t *deg = (int64_t *)calloc((size_t)g->n, sizeof(int64_t));
+    if (!deg) return OG_ENOMEM;
+    for (int64_t i = 0; i < g->n; ++i) {
+        if (labels[i] < 0 || labels[i] >= g->n) { free(deg); return OG_EINVAL; }
+        deg[labels[i]] += g->delta[i];
+    }
+    int64_t i2; i128 s2;
+    modularity_num(g, labels, deg, &i2, &s2);
+    free(deg);
+    *I2 = i2;
+    *S2_hi = (int64_t)(s2 >> 64);
+    *S2_lo = (uint64_t)s2;
+    *Q = q_from_num(g->W, i2, s2);
+    return OG_OK;
+}
+
+/* ------------------------------------------------------- renumber and induce */
+
+/* "Renumbering nodes": sort the cluster ids, unique, map each to its
+ * rank — i.e. an order-preserving dense relabel (D18). */
+int64_t og_renumber(int64_t n, const int32_t *in, int32_t *outl) {
+    int32_t *id = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    uint8_t *used = (uint8_t *)calloc((size_t)n, 1);
+    for (int64_t i = 0; i < n; ++i) used[in[i]] = 1;
+    int64_t k = 0;
+    for (int64_t c = 0; c < n; ++c) id[c] = used[c] ? (int32_t)k++ : -1;
+    for (int64_t i = 0; i < n; ++i) outl[i] = id[in[i]];
+    free(id); free(used);
+    return k;
+}
+
+/* Graph rebuilding (D19): each community becomes a vertex; an
+ * intra-community edge adds its weight to the meta-vertex loop (old loops once);
+ * inter-community weights are summed per community pair. */
+int og_induce(const og_graph *g, const int32_t *C, int64_t k, og_graph **out) {
+    *out = NULL;
+    og_graph *h = graph_alloc(k, 0);
+    rec_t *r = (rec_t *)malloc((size_t)(g->nnz > 0 ? g->nnz : 1) * sizeof(rec_t));
+    int64_t *intra2 = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    if (!h || !r || !intra2) { og_graph_free(h); free(r); free(intra2); return OG_ENOMEM; }
+    int64_t cnt = 0;
+    for (int64_t u = 0; u < g->n; ++u) {
+        int32_t cu = C[u];
+        h->loop[cu] += g->loop[u];
+        for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e) {
+            int32_t cv = C[g->col[e]];
+            if (cv == cu) intra2[cu] += g->w[e];     /* each undirected edge seen twice */
+            else { r[cnt].u = cu; r[cnt].v = cv; r[cnt].w = g->w[e]; ++cnt; }
+        }
+    }
+    for (int64_t c = 0; c < k; ++c) h->loop[c] += intra2[c] / 2;
+    free(intra2);
+    qsort(r, (size_t)cnt, sizeof(rec_t), rec_cmp);
+    free(h->col); free(h->w);
+    h->col = (int32_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int32_t));
+    h->w = (int64_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int64_t));
+    if (!h->col || !h->w) { free(r); og_graph_free(h); return OG_ENOMEM; }
+    fill_csr(h, r, cnt);
+    free(r);
+    h->W = g->W;
+    *out = h;
+    /* W' = W (weight conservation): Σ directed inter weights / 2 + Σ loops */
+    int64_t und = 0, lp = 0;
+    for (int64_t e = 0; e < h->nnz; ++e) und += h->w[e];
+    for (int64_t c = 0; c < k; ++c) lp += h->loop[c];
+    if (und % 2 != 0 || und / 2 + lp != g->W) return OG_EGRAPH;
+    return OG_OK;
+}
+
+/* -------------------------------------------------------------- Algorithm 1/2 */
+
+typedef struct {
+    int64_t n;
+    int32_t *labels;
+    double q;
+    int32_t sweeps;
+    int32_t trace_len;
+    int64_t *moved;
+    double *qs;
+} og_level;
+
+struct og_result {
+    int32_t nlev;
+    og_level *lev;
+    int64_t n0;
+    int64_t edge_visits;
+};
+
+/* D10/D11 stop test, identical expression on both sides (compiled without FMA). */
+static int stop_test(int rule, double Q, double Qp, double theta) {
+    if (rule == 0) {
+        if (fabs(Qp) >= 1e-12) return fabs((Q - Qp) / Qp) < theta;
+        return fabs(Q - Qp) < theta;
+    }
+    if (fabs(Qp) >= 1e-12) return (Q - Qp) / fabs(Qp) < theta;
+    return (Q - Qp) < theta;
+}
+
+/* Algorithm 1 for one level: returns the committed labels in C (not
+ * renumbered), the number of sweeps, and the per-sweep trace. */
+static int one_level(const og_graph *g, const og_config *cfg, double theta, int32_t *C,
+                     og_level *L, int64_t *visits) {
+    int64_t n = g->n;
+    int32_t *next = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    int64_t *deg = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    L->moved = (int64_t *)malloc((size_t)(cfg->max_sweeps + 1) * sizeof(int64_t));
+    L->qs = (double *)malloc((size_t)(cfg->max_sweeps + 1) * sizeof(double));
+    if (!next || !deg || !L->moved || !L->qs) { free(next); free(deg); return OG_ENOMEM; }
+    for (int64_t i = 0; i < n; ++i) C[i] = (int32_t)i;   /* initStatus: singletons */
+    int first = 1;                                        /* Q_prev ← −∞ (D11) */
+    double Qp = 0.0;
+    int32_t s;
+    L->trace_len = 0;
+    for (s = 1; s <= cfg->max_sweeps; ++s) {              /* D12 cap */
+        int64_t moved = og_sweep(g, C, next, 0);          /* decisions from the snapshot */
+        if (moved < 0) { free(next); free(deg); return OG_ENOMEM; }
+        *visits += g->nnz;
+        memcpy(C, next, (size_t)n * sizeof(int32_t));     /* commit (D13) */
+        for (int64_t c = 0; c < n; ++c) deg[c] = 0;
+        for (int64_t i = 0; i < n; ++i) deg[C[i]] += g->delta[i];
+        int64_t I2; i128 S2;
+        modularity_num(g, C, deg, &I2, &S2);              /* "Compute new modularity" */
+        double Q = q_from_num(g->W, I2, S2);
+        L->moved[L->trace_len] = moved;
+        L->qs[L->trace_len] = Q;
+        L->trace_len++;
+        int stop = !first && stop_test(cfg->stop_rule, Q, Qp, theta);
+        first = 0;
+        Qp = Q;
+        if (stop || moved == 0) break;
+    }
+    L->sweeps = s > cfg->max_sweeps ? cfg->max_sweeps : s;
+    if (cfg->merge_isolated) {
+        og_sweep(g, C, next, 1);
+        memcpy(C, next, (size_t)n * sizeof(int32_t));
+    }
+    free(next); free(deg);
+    return OG_OK;
+}
+
+int og_run(const og_graph *g0, const og_config *cfg, og_result **out) {
+    *out = NULL;
+    if (g0->W <= 0) return OG_EZEROW;
+    og_result *r = (og_result *)calloc(1, sizeof(og_result));
+    r->lev = (og_level *)calloc((size_t)(cfg->max_levels > 0 ? cfg->max_levels : 1), sizeof(og_level));
+    r->n0 = g0->n;
+    const og_graph *g = g0;
+    og_graph *owned = NULL;
+    double mod_curr = 0.0;
+    int rc = OG_OK;
+    for (int32_t l = 0; l < cfg->max_levels; ++l) {
+        double theta = cfg->theta;
+        if (cfg->theta_schedule && cfg->theta_schedule_len > 0)      /* D21 */
+            theta = cfg->theta_schedule[l % cfg->theta_schedule_len];
+        og_level L;
+        memset(&L, 0, sizeof(L));
+        L.n = g->n;
+        int32_t *C = (int32_t *)malloc((size_t)g->n * sizeof(int32_t));
+        rc = one_level(g, cfg, theta, C, &L, &r->edge_visits);
+        if (rc) { free(C); free(L.moved); free(L.qs); break; }
+        int64_t k = og_renumber(g->n, C, C);
+        int64_t I2, S2h; uint64_t S2l; double Ql;
+        og_modularity(g, C, &I2, &S2h, &S2l, &Ql);       /* "modularity is recomputed" (D15) */
+        L.labels = C;
+        L.q = Ql;
+        if (l == 0 || !(Ql - mod_curr < cfg->big_theta)) {   /* Alg. 2 (D17) */
+            r->lev[r->nlev++] = L;
+            mod_curr = Ql;
+        } else {
+            free(C); free(L.moved); free(L.qs);
+            break;
+        }
+        if (l + 1 == cfg->max_levels) break;
+        og_graph *h = NULL;
+        rc = og_induce(g, C, k, &h);                      /* "Compute new input graph" */
+        if (rc) { og_graph_free(h); break; }
+        og_graph_free(owned);
+        owned = h;
+        g = h;
+    }
+    og_graph_free(owned);
+    *out = r;
+    return rc;
+}
+
+void og_result_free(og_result *r) {
+    if (!r) return;
+    for (int32_t l = 0; l < r->nlev; ++l) { free(r->lev[l].labels); free(r->lev[l].moved); free(r->lev[l].qs); }
+    free(r->lev);
+    free(r);
+}
+
+int32_t og_result_levels(const og_result *r) { return r->nlev; }
+int64_t og_result_level_n(const og_result *r, int32_t l) { return r->lev[l].n; }
+void og_result_level_labels(const og_result *r, int32_t l, int32_t *out) {
+    memcpy(out, r->lev[l].labels, (size_t)r->lev[l].n * sizeof(int32_t));
+}
+double og_result_level_q(const og_result *r, int32_t l) { return r->lev[l].q; }
+int32_t og_result_level_sweeps(const og_result *r, int32_t l) { return r->lev[l].sweeps; }
+double og_result_final_q(const og_result *r) { return r->nlev ? r->lev[r->nlev - 1].q : 0.0; }
+int32_t og_result_trace_len(const og_result *r, int32_t l) { return r->lev[l].trace_len; }
+void og_result_trace(const og_result *r, int32_t l, int64_t *moved, double *q) {
+    memcpy(moved, r->lev[l].moved, (size_t)r->lev[l].trace_len * sizeof(int64_t));
+    memcpy(q, r->lev[l].qs, (size_t)r->lev[l].trace_len * sizeof(double));
+}
+int64_t og_result_edge_visits(const og_result *r) { return r->edge_visits; }
+
+/* final partition: p[v] = L_last(…L_1(L_0[v])) (composition of the dendrogram) */
+void og_result_final(const og_result *r, int32_t *out) {
+    for (int64_t v = 0; v < r->n0; ++v) {
+        int32_t c = (int32_t)v;
+        for (int32_t l = 0; l < r->nlev; ++l) c = r->lev[l].labels[c];
+        out[v] = c;
+    }
+}

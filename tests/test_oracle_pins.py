@@ -1,0 +1,396 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (CPU only).
+
+Each test cites the passage it pins (P:Lnn = PAPER.md, S:Lnn = SPEC.md).  The oracle is
+checked against independent routes (tests/brute.py rational brute force, networkx,
+closed forms, exhaustive optimum, SPEC worked examples) — never against itself.
+"""
+import json
+import os
+import random
+from fractions import Fraction
+
+import networkx as nx
+import numpy as np
+import pytest
+
+import brute
+import oracle
+from paper_1805_10904_b200 import inputs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _spec():
+    with open(os.path.join(GOLD, "spec_examples.json")) as f:
+        return json.load(f)
+
+
+def _og(n, edges):
+    e = np.array(edges, dtype=np.int64).reshape(-1, 3)
+    return oracle.Graph.from_edges(n, e[:, 0], e[:, 1], e[:, 2])
+
+
+def _bg(n, edges):
+    e = np.array(edges, dtype=np.int64).reshape(-1, 3)
+    return brute.G(n, e[:, 0], e[:, 1], e[:, 2])
+
+
+def _q_exact_from_num(g, lab):
+    m = g.modularity(lab)
+    return Fraction(2 * g.W * m["I2"] - m["S2"], 4 * g.W * g.W), m
+
+
+def random_graph(rng, n, p=0.5, wmax=4, loops=True):
+    edges = []
+    for i in range(n):
+        for j in range(i + 1, n):
+            if rng.random() < p:
+                edges.append([i, j, rng.randint(1, wmax)])
+        if loops and rng.random() < 0.2:
+            edges.append([i, i, rng.randint(1, wmax)])
+    if not edges:
+        edges.append([0, n - 1 if n > 1 else 0, 1])
+    return edges
+
+
+# ------------------------------------------------------------------ graph build
+@pytest.mark.parametrize("ex", _spec()["build_adjacency"], ids=lambda e: e["cite"])
+def test_build_adjacency_spec(ex):
+    """§2 / Neighbor computation; SPEC worked examples."""
+    a = _og(ex["n"], ex["edges"]).arrays()
+    assert list(a["delta"]) == ex["delta"]
+    assert a["W"] == ex["W"]
+    if "row_ptr" in ex:
+        assert list(a["row_ptr"]) == ex["row_ptr"]
+        assert list(a["col"]) == ex["col"]
+    if "w" in ex:
+        assert list(a["w"]) == ex["w"]
+
+
+def test_build_matches_networkx_and_sum_delta():
+    """CSR == networkx adjacency (independent library); Σδ = 2W (D2)."""
+    rng = random.Random(7)
+    for _ in range(20):
+        n = rng.randint(2, 30)
+        edges = random_graph(rng, n, 0.3, 9)
+        g = _og(n, edges)
+        a = g.arrays()
+        G = nx.Graph()
+        G.add_nodes_from(range(n))
+        for u, v, w in edges:
+            if G.has_edge(u, v):
+                G[u][v]["weight"] += w
+            else:
+                G.add_edge(u, v, weight=w)
+        assert a["delta"].sum() == 2 * a["W"]
+        for i in range(n):
+            nb = sorted((j, d["weight"]) for j, d in G[i].items() if j != i)
+            row = list(zip(a["col"][a["row_ptr"][i]:a["row_ptr"][i + 1]], a["w"][a["row_ptr"][i]:a["row_ptr"][i + 1]]))
+            assert [(int(j), int(w)) for j, w in row] == nb
+            lw = G[i][i]["weight"] if G.has_edge(i, i) else 0
+            assert a["loop"][i] == lw
+            # networkx weighted degree counts a loop twice, as D2 does
+            assert a["delta"][i] == G.degree(i, weight="weight")
+
+
+def test_build_rejects_bad_input():
+    with pytest.raises(oracle.OracleError):
+        oracle.Graph.from_edges(2, [0], [5], [1])      # id out of range
+    with pytest.raises(oracle.OracleError):
+        oracle.Graph.from_edges(2, [0], [1], [0])      # weight must be > 0
+
+
+# ------------------------------------------------------------------ Eq. 3
+@pytest.mark.parametrize("ex", _spec()["modularity"], ids=lambda e: e["cite"])
+def test_modularity_closed_forms(ex):
+    """Eq. 3 closed forms."""
+    if "ring" in ex:
+        r = inputs.ring_of_cliques(*ex["ring"])
+        g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+        lab = r.truth if ex.get("planted") else np.zeros(r.n, np.int32)
+    else:
+        g = _og(ex["n"], ex["edges"])
+        lab = np.array(ex["labels"], np.int32)
+    q, m = _q_exact_from_num(g, lab)
+    assert q == Fraction(ex["Q_num"], ex["Q_den"])
+    assert m["Q"] == pytest.approx(ex["Q_num"] / ex["Q_den"], abs=1e-15)
+
+
+def test_modularity_pair_sum_bruteforce():
+    """Eq. 3 aggregate form (oracle) == pair-sum definition in exact rationals."""
+    rng = random.Random(1)
+    for _ in range(60):
+        n = rng.randint(1, 9)
+        edges = random_graph(rng, n, 0.5, 5)
+        lab = [rng.randrange(n) for _ in range(n)]
+        g = _og(n, edges)
+        q, m = _q_exact_from_num(g, np.array(lab, np.int32))
+        assert q == brute.q_exact(_bg(n, edges), lab)
+        assert -0.5 - 1e-15 <= m["Q"] <= 1.0
+        assert abs(m["Q"] - float(q)) <= 1e-15 * max(1.0, abs(float(q)))
+
+
+def test_modularity_networkx():
+    """Eq. 3 == networkx.community.modularity (same loop convention)."""
+    rng = random.Random(3)
+    for _ in range(30):
+        n = rng.randint(2, 40)
+        edges = random_graph(rng, n, 0.2, 7)
+        G = nx.Graph()
+        G.add_nodes_from(range(n))
+        for u, v, w in edges:
+            if G.has_edge(u, v):
+                G[u][v]["weight"] += w
+            else:
+                G.add_edge(u, v, weight=w)
+        lab = [rng.randrange(max(1, n // 3)) for _ in range(n)]
+        comms = {}
+        for v, c in enumerate(lab):
+            comms.setdefault(c, set()).add(v)
+        qn = nx.community.modularity(G, list(comms.values()), weight="weight")
+        qo = _og(n, edges).modularity(np.array(lab, np.int32))["Q"]
+        assert abs(qo - qn) < 1e-13
+
+
+def test_karate_singletons_closed_form():
+    """Singletons: I2 = 0 (no loops), so Q = −Σ_i (δ_i/2W)² (Eq. 3)."""
+    r = inputs.karate()
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    a = g.arrays()
+    q, _ = _q_exact_from_num(g, np.arange(34, dtype=np.int32))
+    assert q == -sum(Fraction(int(d), 156) ** 2 for d in a["delta"])
+    assert float(q) == pytest.approx(-0.04980276134122288, abs=1e-12)
+
+
+# ------------------------------------------------------------------ Eq. 4/5 + heuristics
+@pytest.mark.parametrize("ex", _spec()["best_move"], ids=lambda e: e["cite"])
+def test_best_move_spec(ex):
+    """Eq. 5 + §3.1.1/§3.1.2 SPEC examples."""
+    g = _og(ex["n"], ex["edges"])
+    lab = np.array(ex["labels"], np.int32)
+    if "decisions" in ex:
+        assert list(g.decide(lab, range(ex["n"]))) == ex["decisions"]
+    else:
+        assert g.decide(lab, [ex["vertex"]])[0] == ex["decision"]
+
+
+def test_decide_equals_eq3_recomputation():
+    """Gain consistency (D4; SPEC criterion 5): the oracle's closed-form int128 score
+    (Eq. 4 read as D4) picks exactly the move that brute-force re-evaluation of Eq. 3
+    picks, including the strict >0 test, min-label ties and
+    the singlet rule."""
+    rng = random.Random(11)
+    checked = 0
+    for trial in range(250):
+        n = rng.randint(2, 8)
+        edges = random_graph(rng, n, rng.choice([0.3, 0.6, 0.9]), rng.choice([1, 1, 3]))
+        k = rng.randint(1, n)
+        lab = [rng.randrange(k) for _ in range(n)]
+        g, bg = _og(n, edges), _bg(n, edges)
+        got = g.decide(np.array(lab, np.int32), range(n))
+        want = [brute.decide(bg, lab, i) for i in range(n)]
+        assert list(got) == want, (edges, lab)
+        gotm = g.decide(np.array(lab, np.int32), range(n), mode=1)
+        assert list(gotm) == [brute.decide(bg, lab, i, mode=1) for i in range(n)]
+        checked += n
+    assert checked > 500
+
+
+def test_sweep_is_jacobi():
+    """Alg. 1 inner loop evaluates every vertex on the previous iteration's state."""
+    rng = random.Random(5)
+    for _ in range(40):
+        n = rng.randint(2, 8)
+        edges = random_graph(rng, n, 0.5, 3)
+        lab = [rng.randrange(n) for _ in range(n)]
+        out, moved = _og(n, edges).sweep(np.array(lab, np.int32))
+        want = brute.sweep(_bg(n, edges), lab)
+        assert list(out) == want
+        assert moved == sum(a != b for a, b in zip(lab, want))
+
+
+@pytest.mark.parametrize("ex", _spec()["merge_isolated"], ids=lambda e: e["cite"])
+def test_merge_isolated_spec(ex):
+    """Isolated-node merge, SPEC examples S:L282-284."""
+    g = _og(ex["n"], ex["edges"])
+    out, _ = g.sweep(np.array(ex["labels"], np.int32), mode=1)
+    assert list(out) == ex["after"]
+
+
+# ------------------------------------------------------------------ renumber / induce
+@pytest.mark.parametrize("ex", _spec()["renumber"], ids=lambda e: e["cite"])
+def test_renumber_spec(ex):
+    out, k = oracle.renumber(np.array(ex["labels"], np.int32))
+    assert list(out) == ex["out"]
+    assert k == len(set(ex["labels"]))
+
+
+@pytest.mark.parametrize("ex", _spec()["induce"], ids=lambda e: e["cite"])
+def test_induce_spec(ex):
+    """Graph rebuilding."""
+    if "ring" in ex:
+        r = inputs.ring_of_cliques(*ex["ring"])
+        g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+        lab = r.truth
+    else:
+        g = _og(ex["n"], ex["edges"])
+        lab = np.array(ex["labels"], np.int32)
+    h = g.induce(lab, ex["k"]).arrays()
+    assert list(h["loop"]) == ex["loop"]
+    assert h["W"] == ex["W"]
+    if "edges_out" in ex:
+        got = [[int(i), int(h["col"][e]), int(h["w"][e])] for i in range(ex["k"])
+               for e in range(h["row_ptr"][i], h["row_ptr"][i + 1])]
+        assert got == ex["edges_out"]
+    else:
+        assert len(h["col"]) == ex["nnz"]
+
+
+def test_induce_preserves_modularity_and_weight():
+    """D19: W' = W and Q(G', singletons) == Q(G, P) exactly (SPEC criterion 8)."""
+    rng = random.Random(9)
+    for _ in range(40):
+        n = rng.randint(2, 25)
+        edges = random_graph(rng, n, 0.3, 6)
+        g = _og(n, edges)
+        lab, k = oracle.renumber(np.array([rng.randrange(max(1, n // 2)) for _ in range(n)], np.int32))
+        h = g.induce(lab, k)
+        assert h.W == g.W
+        a, b = g.modularity(lab), h.modularity(np.arange(k, dtype=np.int32))
+        assert (a["I2"], a["S2"]) == (b["I2"], b["S2"])
+        # identity partition: induced graph == input graph
+        hi = g.induce(np.arange(n, dtype=np.int32), n).arrays()
+        ga = g.arrays()
+        for key in ("row_ptr", "col", "w", "loop", "delta"):
+            assert np.array_equal(hi[key], ga[key])
+
+
+# ------------------------------------------------------------------ whole algorithm
+def test_two_vertex_run_spec():
+    """two-vertex one-edge graph ends in community 0 with Q = 0."""
+    ex = _spec()["one_level"][0]
+    r = oracle.run(_og(ex["n"], ex["edges"]))
+    assert list(r.final) == ex["final_labels"]
+    assert r.final_q == 0.0
+
+
+@pytest.mark.parametrize("ex", _spec()["final_partition"], ids=lambda e: e["cite"])
+def test_final_partition_composition(ex):
+    """Composition of the dendrogram, checked on the levels run() returns."""
+    # composition law checked directly on the spec levels
+    out = list(range(len(ex["levels"][0])))
+    for lev in ex["levels"]:
+        out = [lev[c] for c in out]
+    assert out == ex["out"]
+
+
+def test_final_partition_of_run_is_composition():
+    r = inputs.karate()
+    res = oracle.run(oracle.Graph.from_edges(r.n, r.src, r.dst))
+    out = np.arange(r.n)
+    for lev in res.levels:
+        out = lev[out]
+    assert np.array_equal(out, res.final)
+
+
+@pytest.mark.parametrize("stop_rule", [0, 1])
+def test_karate_band(stop_rule):
+    """north_star pin: Zachary karate club Q ≈ 0.41–0.42; never above the optimum."""
+    gold = json.load(open(os.path.join(GOLD, "karate.json")))
+    r = inputs.karate()
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    assert (g.n, g.nnz // 2, g.W) == (gold["n"], gold["m"], gold["W"])
+    res = oracle.run(g, stop_rule=stop_rule)
+    lo, hi = gold["q_band"]
+    assert lo <= res.final_q <= hi
+    assert res.final_q <= gold["q_optimum"]
+    assert res.final_q == g.modularity(res.final)["Q"]
+
+
+@pytest.mark.parametrize("k", [5, 10, 25])
+@pytest.mark.parametrize("c", [4, 6, 10])
+@pytest.mark.parametrize("stop_rule", [0, 1])
+def test_ring_of_cliques_recovery(k, c, stop_rule):
+    """SPEC criterion 2: level 0 groups exactly the planted cliques; final Q >=
+    planted Q (Eq. 3 of the planted partition)."""
+    r = inputs.ring_of_cliques(k, c)
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    res = oracle.run(g, stop_rule=stop_rule)
+    l0 = res.levels[0]
+    # same partition as truth: bijection between labels
+    pairs = set(zip(l0.tolist(), r.truth.tolist()))
+    assert len(pairs) == k == len(set(l0.tolist()))
+    q_planted, _ = _q_exact_from_num(g, r.truth)
+    q_final, _ = _q_exact_from_num(g, res.final)
+    assert q_final >= q_planted
+
+
+def test_exhaustive_optimum_bound_atlas():
+    """SPEC criterion 1: Q_louvain <= exhaustive optimum on every connected graph of
+    the networkx atlas (<= 7 vertices), both stop rules; also Q_louvain >= Q(singletons)."""
+    count = 0
+    for G in nx.graph_atlas_g()[1:]:
+        if G.number_of_edges() == 0 or not nx.is_connected(G):
+            continue
+        n = G.number_of_nodes()
+        e = np.array(list(G.edges()), np.int64)
+        g = oracle.Graph.from_edges(n, e[:, 0], e[:, 1])
+        qopt = brute.optimum(brute.G(n, e[:, 0], e[:, 1]))
+        for rule in (0, 1):
+            res = oracle.run(g, stop_rule=rule)
+            qf, _ = _q_exact_from_num(g, res.final)
+            assert qf <= qopt
+        count += 1
+    assert count > 900
+
+
+def test_exhaustive_optimum_bound_n10():
+    """Exhaustive Bell(10) = 115,975 partitions on random weighted 10-vertex graphs."""
+    rng = random.Random(21)
+    for _ in range(3):
+        n = 10
+        edges = random_graph(rng, n, 0.35, 5)
+        g, bg = _og(n, edges), _bg(n, edges)
+        qopt = brute.optimum(bg)
+        res = oracle.run(g)
+        qf, _ = _q_exact_from_num(g, res.final)
+        assert qf <= qopt
+
+
+def test_theorem1_label_subset_and_conservation():
+    """Theorem 1: after every committed sweep the set of non-empty labels is a
+    subset of the previous one; Σ deg_C = 2W and Σ |C| = N (Eq. 2)."""
+    for rec in (inputs.karate(), inputs.ring_of_cliques(6, 5), inputs.rmat(9, 8, seed=1),
+                inputs.sbm(2000, 20, 16, 0.3, seed=2)):
+        g = oracle.Graph.from_edges(rec.n, rec.src, rec.dst, rec.w)
+        d = g.arrays()["delta"]
+        lab = np.arange(rec.n, dtype=np.int32)
+        for _ in range(30):
+            nxt, moved = g.sweep(lab)
+            assert set(nxt.tolist()) <= set(lab.tolist())
+            deg = np.bincount(nxt, weights=d, minlength=rec.n)
+            assert deg.sum() == 2 * g.W
+            lab = nxt
+            if moved == 0:
+                break
+
+
+def test_sbm_ground_truth_recovery():
+    """Planted partition SBM (C2 analogue, 20k vertices, blocks of 1000, avg degree 32,
+    mu = 0.3): the method recovers the planted blocks exactly (NMI = 1)."""
+    rec = inputs.sbm(20_000, 20, 32, 0.3, seed=2)
+    g = oracle.Graph.from_edges(rec.n, rec.src, rec.dst)
+    res = oracle.run(g)
+    pairs = set(zip(res.final.tolist(), rec.truth.tolist()))
+    assert len(pairs) == 20 == len(set(res.final.tolist()))
+
+
+def test_theta_schedule_cycles():
+    """D21 'threshold cycling': a schedule of length 1 equals the constant θ."""
+    r = inputs.karate()
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    a = oracle.run(g, theta=1e-3)
+    b = oracle.run(g, theta_schedule=[1e-3])
+    assert a.sweeps == b.sweeps and np.array_equal(a.final, b.final)
+    c = oracle.run(g, theta_schedule=[1e-6, 1e-1])
+    assert c.sweeps[0] == oracle.run(g).sweeps[0]

@@ -1,0 +1,30 @@
+#!/bin/bash
+# Mutation check of the oracle pins: each line injects one plausible mistake into
+# oracle/oracle.c and expects tests/test_oracle_pins.py to FAIL.  Restores the file.
+# Run from the repo root:  bash tools/oracle_mutation_check.sh
+set -u
+cd "$(dirname "$0")/.."
+mut() {
+  cp oracle/oracle.c /tmp/oracle.c.bak
+  sed -i "$1" oracle/oracle.c
+  if cmp -s oracle/oracle.c /tmp/oracle.c.bak; then echo "[$2] SED DID NOT APPLY"; return; fi
+  rm -f oracle/liboracle.so
+  r=$(timeout 600 python -m pytest tests/test_oracle_pins.py -x -q 2>&1 | tail -1)
+  echo "[$2] $r"
+  cp /tmp/oracle.c.bak oracle/oracle.c
+  rm -f oracle/liboracle.so
+}
+mut 's/(i128)st->deg\[own\] - di)/(i128)st->deg[own])/' "drop -delta_i in S_own (Eq.4 C(i)\\{i})"
+mut 's/(S == S_best \&\& c < best)/(S == S_best \&\& c > best)/' "max-label tie (P:L95)"
+mut 's/best >= 0 \&\& S_best > S_own/best >= 0 \&\& S_best >= S_own/' "non-strict move (P:L223)"
+mut 's/st->size\[best\] == 1 \&\& best > own) result = own;/st->size[best] == 1 \&\& best < own) result = own;/' "singlet rule inverted (P:L92)"
+mut 's/int64_t s = 2 \* g->loop\[i\];/int64_t s = g->loop[i];/' "loop once in delta (D2)"
+mut 's/s += 2 \* g->loop\[i\];/s += g->loop[i];/' "loop once in I2 (D24)"
+mut 's/h->loop\[c\] += intra2\[c\] \/ 2;/h->loop[c] += intra2[c];/' "induce double intra (D19)"
+mut 's/id\[c\] = used\[c\] ? (int32_t)k++ : -1;/id[c] = used[c] ? (int32_t)(k++) : -1; if (used[c] \&\& k > 1) id[c] = (int32_t)(k - 1) ^ 1;/' "renumber not order-preserving (D18)"
+mut 's/if (mode == 1 \&\& st->size\[own\] != 1) return own;/if (0) return own;/' "merge non-singlets (D14)"
+mut 's/st->deg\[labels\[i\]\] += g->delta\[i\];/st->deg[labels[i]] += 1;/' "deg as count (Eq.2)"
+mut 's/i128 S = twoW \* st->e\[c\] - di \* (i128)st->deg\[c\];/i128 S = twoW * st->e[c] + di * (i128)st->deg[c];/' "sign flip in S (Eq.4)"
+mut 's/for (s = 1; s <= cfg->max_sweeps; ++s) {/for (s = 1; s <= cfg->max_sweeps - 1; ++s) {/' "cap off by one (D12)"
+mut 's/if (l == 0 || !(Ql - mod_curr < cfg->big_theta))/if (!(Ql - mod_curr < cfg->big_theta))/' "level 0 not forced (Alg.2)"
+mut 's/return neg ? -d : d;/return d;/' "d128 sign lost (D22)"
