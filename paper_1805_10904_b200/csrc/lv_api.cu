@@ -1,0 +1,770 @@
+// lv_api.cu — C ABI of liblouvain (include/louvain.h) and the host orchestration of
+// Algorithm 2 around Algorithm 1.
+//
+// Per level: init status -> local-move sweeps with fused Eq. 3 numerators
+// -> stop test (D10-D13) -> isolated merge -> renumber ->
+// contract -> level Q and the Θ test (D17).
+//
+// Fused stop test: sweep s+1 reads the committed state s and emits, for
+// free, that state's exact Eq. 3 numerators (Σ e_{i->C(i)} and Σ deg_C²).  The host then
+// evaluates Alg. 1's test for state s; if it fires, sweep s+1's tentative decisions are
+// dropped (never committed) — identical to "commit s, recompute Q, test" of the literal
+// algorithm, without a separate edge pass per sweep.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "lv_graph.cuh"
+
+using namespace lv;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// D22 (refined): pinned int128 -> fp64 on the magnitude.
+double d128(i128 x) {
+  const bool neg = x < 0;
+  const u128 m = neg ? (u128)(-x) : (u128)x;
+  const u64 hi = (u64)(m >> 64), lo = (u64)m;
+  const double d = (double)hi * 18446744073709551616.0 + (double)lo;
+  return neg ? -d : d;
+}
+
+// Eq. 3 from exact numerators: Q = d(2W·I2 − S2) / d(4W²).
+double q_from(i64 W, i128 I2, i128 S2) {
+  const i128 num = (i128)2 * W * I2 - S2;
+  const i128 den = (i128)4 * W * W;
+  return d128(num) / d128(den);
+}
+
+// Alg. 1 stop test with readings D10/D11.
+bool stop_test(int rule, double Q, double Qp, double theta) {
+  if (rule == 0) {
+    if (std::fabs(Qp) >= 1e-12) return std::fabs((Q - Qp) / Qp) < theta;
+    return std::fabs(Q - Qp) < theta;
+  }
+  if (std::fabs(Qp) >= 1e-12) return (Q - Qp) / std::fabs(Qp) < theta;
+  return (Q - Qp) < theta;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_init_state(i64 n, int32_t *l0, int32_t *l1, i64 *deg, int32_t *size, const i64 *delta) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    l0[i] = (int32_t)i;
+    l1[i] = (int32_t)i;
+    deg[i] = delta[i];
+    size[i] = 1;
+  }
+}
+
+__global__ void k_state_from_labels(i64 n, const int32_t *lab, const i64 *delta, i64 *deg, int32_t *size, int *err) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    const int32_t c = lab[i];
+    if (c < 0 || c >= n) { atomicOr(err, 1); continue; }
+    atomicAdd((u64 *)&deg[c], (u64)delta[i]);
+    atomicAdd(&size[c], 1);
+  }
+}
+
+__global__ void k_copy_i32(i64 n, const int32_t *a, int32_t *b) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) b[i] = a[i];
+}
+
+__global__ void k_compose(i64 n, int32_t *p, const int32_t *lev) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) p[i] = lev[p[i]];
+}
+
+struct LoopArr {
+  const i64 *a;
+  __device__ __forceinline__ u64 operator()(i64 i) const { return (u64)a[i]; }
+};
+struct InactiveDelta {  // δ_i of vertices without non-loop neighbours (else 0)
+  const i64 *rp, *delta;
+  __device__ __forceinline__ i64 operator()(i64 i) const { return rp[i + 1] == rp[i] ? delta[i] : 0; }
+};
+struct DegArr {
+  const i64 *a;
+  __device__ __forceinline__ i64 operator()(i64 i) const { return a[i]; }
+};
+
+template <class T>
+__global__ void k_to_i64(i64 n, const T *a, i64 *b) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) b[i] = (i64)a[i];
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct LevelRec {
+  i64 n = 0;
+  Buf<int32_t> labels;  // dense, values in [0, n_{l+1})
+  double q = 0;
+  int32_t sweeps = 0;
+  double times[5] = {0, 0, 0, 0, 0};
+};
+
+struct louvain_ctx {
+  Ctx c;
+  bool own_stream = false;
+  louvain_config cfg;
+  std::vector<double> sched;
+  DGraph g0;
+  double csr_ms = 0;
+  std::vector<std::unique_ptr<LevelRec>> levels;
+  Buf<int32_t> final_part;
+  bool ran = false;
+  std::string err;
+  i64 edge_visits = 0;
+  i64 run_launches = 0;
+  u64 *hctr = nullptr;         // pinned host copy of the sweep counters
+  Buf<u64> dctr;               // NBIN x 8 device counters
+  std::unique_ptr<Bins> vb0;   // level-0 vertex bins (step-level API)
+  ~louvain_ctx() {
+    levels.clear();
+    final_part.release();
+    vb0.reset();
+    dctr.release();
+    g0 = DGraph();
+    if (c.s) cudaStreamSynchronize(c.s);
+    if (hctr) cudaFreeHost(hctr);
+    if (own_stream && c.s) cudaStreamDestroy(c.s);
+  }
+};
+
+namespace {
+
+// Per-level community state: double-buffered labels (snapshot / next), deg_C, |C|.
+struct State {
+  Buf<int32_t> lab[2];
+  Buf<i64> deg;
+  Buf<int32_t> size;
+  int cur = 0;
+};
+
+struct SweepOut {
+  u64 i2 = 0, moved = 0, cand = 0;
+  u128 s2 = 0;
+};
+
+// Run one pass of MODE over the bins of g (snapshot st.lab[cur] -> st.lab[cur^1]).
+SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int mode, KTimer *tm = nullptr,
+                  std::vector<SweepOut> *per_bin = nullptr) {
+  Ctx &c = h->c;
+  LV_CUDA(cudaMemsetAsync(h->dctr.p, 0, NBIN * 8 * sizeof(u64), c.s));
+  AggArgs a;
+  memset(&a, 0, sizeof(a));
+  a.ptr = g.row_ptr.p;
+  a.keys = g.col.p;
+  a.w = g.w.p;
+  a.label = st.lab[st.cur].p;
+  a.label_next = st.lab[st.cur ^ 1].p;
+  a.deg = st.deg.p;
+  a.size = st.size.p;
+  a.delta = g.delta.p;
+  a.twoW = 2 * g.W;
+  a.counters = h->dctr.p;
+  if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, B, a, tm);
+  else launch_agg_wt<M_MERGE>(c, g.wt, B, a, tm);
+  LV_CUDA(cudaMemcpyAsync(h->hctr, h->dctr.p, NBIN * 8 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  SweepOut o;
+  for (int b = 0; b < NBIN; ++b) {
+    const u64 *x = h->hctr + 8 * b;
+    SweepOut p;
+    p.i2 = x[0];
+    p.moved = x[1];
+    p.s2 = ((u128)x[3] << 64) | x[2];
+    p.cand = x[4];
+    o.i2 += p.i2;
+    o.moved += p.moved;
+    o.s2 += p.s2;
+    o.cand += p.cand;
+    if (per_bin) per_bin->push_back(p);
+  }
+  return o;
+}
+
+void commit(louvain_ctx *h, const DGraph &g, State &st) {
+  Ctx &c = h->c;
+  LV_LAUNCH(c, k_commit, grid_for(c, g.n), 256, 0, g.n, st.lab[st.cur].p, st.lab[st.cur ^ 1].p, g.delta.p, st.deg.p,
+            st.size.p);
+  st.cur ^= 1;
+}
+
+void init_state(louvain_ctx *h, const DGraph &g, State &st) {
+  Ctx &c = h->c;
+  st.lab[0].alloc(c.A, g.n);
+  st.lab[1].alloc(c.A, g.n);
+  st.deg.alloc(c.A, g.n);
+  st.size.alloc(c.A, g.n);
+  st.cur = 0;
+  LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg.p, st.size.p, g.delta.p);
+}
+
+// Level constants: Σ loop and Σ_{inactive} δ² (labels of vertices without neighbours
+// never change and are never adopted, so their deg_C stays δ_i).
+void level_consts(louvain_ctx *h, const DGraph &g, u64 &lsum, u128 &s2_inact) {
+  Ctx &c = h->c;
+  Buf<u64> t(c.A, 4);
+  LV_CUDA(cudaMemsetAsync(t.p, 0, 4 * sizeof(u64), c.s));
+  LV_LAUNCH(c, k_sum_u64<LoopArr>, grid_for(c, g.n), 256, 0, LoopArr{g.loop.p}, g.n, t.p);
+  LV_LAUNCH(c, k_sumsq_u128<InactiveDelta>, grid_for(c, g.n), 256, 0, InactiveDelta{g.row_ptr.p, g.delta.p}, g.n,
+            t.p + 2);
+  u64 ht[4];
+  LV_CUDA(cudaMemcpyAsync(ht, t.p, sizeof(ht), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  lsum = ht[0];
+  s2_inact = ((u128)ht[3] << 64) | ht[2];
+}
+
+// Algorithm 1 for one level.  Returns the number of committed sweeps.
+int32_t one_level(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, double theta) {
+  const louvain_config &cfg = h->cfg;
+  if (cfg.max_sweeps <= 0) return 0;
+  u64 lsum;
+  u128 s2i;
+  level_consts(h, g, lsum, s2i);
+  SweepOut o = run_pass(h, g, B, st, M_SWEEP);
+  h->edge_visits += g.nnz;
+  commit(h, g, st);
+  int32_t sweeps = 1;
+  if (o.moved == 0) return sweeps;
+  bool first = true;
+  double Qp = 0.0;
+  for (int32_t s = 2; s <= cfg.max_sweeps; ++s) {
+    o = run_pass(h, g, B, st, M_SWEEP);  // tentative sweep s; numerators of state s-1
+    h->edge_visits += g.nnz;
+    const i128 I2 = (i128)o.i2 + (i128)2 * (i128)lsum;
+    const i128 S2 = (i128)(o.s2 + s2i);
+    const double Q = q_from(g.W, I2, S2);
+    const bool stop = !first && stop_test(cfg.stop_rule, Q, Qp, theta);
+    first = false;
+    Qp = Q;
+    if (stop) break;  // drop sweep s: the literal algorithm stopped after s-1
+    commit(h, g, st);
+    sweeps = s;
+    if (o.moved == 0) break;
+  }
+  return sweeps;
+}
+
+// Q of the partition that produced graph hgr: I2 = 2Σloop', S2 = Σδ'² (exact).
+double q_of_contracted(louvain_ctx *h, const DGraph &hg) {
+  Ctx &c = h->c;
+  Buf<u64> t(c.A, 4);
+  LV_CUDA(cudaMemsetAsync(t.p, 0, 4 * sizeof(u64), c.s));
+  LV_LAUNCH(c, k_sum_u64<LoopArr>, grid_for(c, hg.n), 256, 0, LoopArr{hg.loop.p}, hg.n, t.p);
+  LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, hg.n), 256, 0, DegArr{hg.delta.p}, hg.n, t.p + 2);
+  u64 ht[4];
+  LV_CUDA(cudaMemcpyAsync(ht, t.p, sizeof(ht), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  return q_from(hg.W, (i128)2 * (i128)ht[0], (i128)(((u128)ht[3] << 64) | ht[2]));
+}
+
+void run_impl(louvain_ctx *h) {
+  Ctx &c = h->c;
+  const louvain_config &cfg = h->cfg;
+  h->levels.clear();
+  h->final_part.release();
+  h->ran = false;
+  h->edge_visits = 0;
+  const i64 l0 = c.launches;
+  std::unique_ptr<DGraph> owned;
+  const DGraph *g = &h->g0;
+  double mod_curr = 0.0;
+  for (int32_t l = 0; l < cfg.max_levels; ++l) {
+    const double theta = h->sched.empty() ? cfg.theta : h->sched[l % h->sched.size()];
+    auto rec = std::make_unique<LevelRec>();
+    rec->n = g->n;
+    rec->times[0] = l == 0 ? h->csr_ms : 0.0;
+    double t0 = now_ms();
+    State st;
+    init_state(h, *g, st);
+    Bins B;
+    build_bins(c, g->row_ptr.p, g->n, g->n, B);
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    double t1 = now_ms();
+    rec->sweeps = one_level(h, *g, B, st, theta);
+    if (cfg.merge_isolated) {
+      run_pass(h, *g, B, st, M_MERGE);
+      commit(h, *g, st);
+    }
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    double t2 = now_ms();
+    rec->labels.alloc(c.A, g->n);
+    Buf<i64> ndelta;
+    const i64 k = renumber(c, g->n, st.lab[st.cur].p, st.size.p, st.deg.p, rec->labels.p, ndelta);
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    double t3 = now_ms();
+    st = State();
+    auto hg = std::make_unique<DGraph>();
+    contract(c, *g, B, rec->labels.p, k, std::move(ndelta), *hg);
+    double t4 = now_ms();
+    rec->q = q_of_contracted(h, *hg);
+    rec->times[1] = t1 - t0;
+    rec->times[2] = t2 - t1;
+    rec->times[3] = t3 - t2;
+    rec->times[4] = t4 - t3;
+    if (l == 0 || !(rec->q - mod_curr < cfg.big_theta)) {  // Alg. 2 (D17)
+      mod_curr = rec->q;
+      h->levels.push_back(std::move(rec));
+    } else {
+      break;
+    }
+    if (l + 1 == cfg.max_levels) break;
+    owned = std::move(hg);
+    g = owned.get();
+  }
+  // compose the final partition (dendrogram composition)
+  const i64 n0 = h->g0.n;
+  h->final_part.alloc(c.A, n0);
+  LV_LAUNCH(c, k_copy_i32, grid_for(c, n0), 256, 0, n0, h->levels[0]->labels.p, h->final_part.p);
+  for (size_t l = 1; l < h->levels.size(); ++l)
+    LV_LAUNCH(c, k_compose, grid_for(c, n0), 256, 0, n0, h->final_part.p, h->levels[l]->labels.p);
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  h->run_launches = c.launches - l0;
+  h->ran = true;
+}
+
+louvain_status fail(louvain_ctx *h, const Error &e) {
+  if (h) h->err = e.msg;
+  else g_create_error = e.msg;
+  return (louvain_status)e.code;
+}
+
+Bins &vbins0(louvain_ctx *h) {
+  if (!h->vb0) {
+    h->vb0 = std::make_unique<Bins>();
+    build_bins(h->c, h->g0.row_ptr.p, h->g0.n, h->g0.n, *h->vb0);
+  }
+  return *h->vb0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+louvain_status louvain_config_default(louvain_config *cfg) {
+  if (!cfg) return LV_EINVAL;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->theta = 1e-6;
+  cfg->big_theta = 1e-6;
+  cfg->max_sweeps = 100;
+  cfg->max_levels = 64;
+  cfg->stop_rule = 0;
+  cfg->merge_isolated = 1;
+  cfg->device = 0;
+  cfg->world = 1;
+  return LV_OK;
+}
+
+louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg_in, louvain_t *out) {
+  if (!out) return LV_EINVAL;
+  *out = nullptr;
+  g_create_error.clear();
+  if (!gr || gr->n <= 0 || gr->m < 0 || (gr->m > 0 && (!gr->src || !gr->dst)) ||
+      (gr->wtype != LV_W_NONE && gr->m > 0 && !gr->w) || gr->wtype < 0 || gr->wtype > 2 || gr->n > 0x7fffffffLL) {
+    g_create_error = "invalid graph arguments";
+    return LV_EINVAL;
+  }
+  louvain_config cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else louvain_config_default(&cfg);
+  if (cfg.max_sweeps < 1 || cfg.max_levels < 1 || cfg.stop_rule < 0 || cfg.stop_rule > 1 || !(cfg.theta >= 0) ||
+      !(cfg.big_theta == cfg.big_theta) || (cfg.theta_schedule_len > 0 && !cfg.theta_schedule)) {
+    g_create_error = "invalid config";
+    return LV_EINVAL;
+  }
+  auto *h = new louvain_ctx();
+  try {
+    h->cfg = cfg;
+    if (cfg.theta_schedule_len > 0) h->sched.assign(cfg.theta_schedule, cfg.theta_schedule + cfg.theta_schedule_len);
+    h->cfg.theta_schedule = nullptr;
+    LV_CUDA(cudaSetDevice(cfg.device));
+    h->c.device = cfg.device;
+    LV_CUDA(cudaDeviceGetAttribute(&h->c.sms, cudaDevAttrMultiProcessorCount, cfg.device));
+    if (cfg.stream) {
+      h->c.s = (cudaStream_t)cfg.stream;
+    } else {
+      LV_CUDA(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    h->c.A.a = cfg.alloc;
+    h->c.A.f = cfg.free;
+    h->c.A.ctx = cfg.alloc_ctx;
+    h->c.A.s = h->c.s;
+    LV_CUDA(cudaMallocHost((void **)&h->hctr, NBIN * 8 * sizeof(u64)));
+    h->dctr.alloc(h->c.A, NBIN * 8);
+    // input to device
+    const int32_t *src = gr->src, *dst = gr->dst;
+    const void *w = gr->w;
+    Buf<int32_t> dsrc, ddst;
+    Buf<unsigned char> dw;
+    const double t0 = now_ms();
+    if (!gr->on_device && gr->m > 0) {
+      dsrc.alloc(h->c.A, gr->m);
+      ddst.alloc(h->c.A, gr->m);
+      LV_CUDA(cudaMemcpyAsync(dsrc.p, gr->src, gr->m * sizeof(int32_t), cudaMemcpyHostToDevice, h->c.s));
+      LV_CUDA(cudaMemcpyAsync(ddst.p, gr->dst, gr->m * sizeof(int32_t), cudaMemcpyHostToDevice, h->c.s));
+      src = dsrc.p;
+      dst = ddst.p;
+      if (gr->wtype != LV_W_NONE) {
+        const size_t wb = gr->wtype == LV_W_I32 ? 4 : 8;
+        dw.alloc(h->c.A, gr->m * wb);
+        LV_CUDA(cudaMemcpyAsync(dw.p, gr->w, gr->m * wb, cudaMemcpyHostToDevice, h->c.s));
+        w = dw.p;
+      }
+    }
+    build_csr(h->c, gr->n, gr->m, src, dst, w, gr->wtype, h->g0);
+    h->csr_ms = now_ms() - t0;
+  } catch (const Error &e) {
+    g_create_error = e.msg;
+    delete h;
+    return (louvain_status)e.code;
+  }
+  *out = h;
+  return LV_OK;
+}
+
+louvain_status louvain_run(louvain_t h) {
+  if (!h) return LV_EINVAL;
+  try {
+    LV_CUDA(cudaSetDevice(h->c.device));
+    run_impl(h);
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+louvain_status louvain_num_levels(louvain_t h, int32_t *levels) {
+  if (!h || !levels) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  *levels = (int32_t)h->levels.size();
+  return LV_OK;
+}
+
+louvain_status louvain_level_size(louvain_t h, int32_t level, int64_t *n) {
+  if (!h || !n) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  if (level < 0 || level >= (int32_t)h->levels.size()) return LV_ERANGE;
+  *n = h->levels[level]->n;
+  return LV_OK;
+}
+
+louvain_status louvain_get_partition(louvain_t h, int32_t level, int32_t *out, int64_t cap, int32_t on_device) {
+  if (!h || !out) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  if (level < -1 || level >= (int32_t)h->levels.size()) return LV_ERANGE;
+  const int32_t *src = level < 0 ? h->final_part.p : h->levels[level]->labels.p;
+  const i64 n = level < 0 ? h->g0.n : h->levels[level]->n;
+  if (cap < n) return LV_EINVAL;
+  try {
+    LV_CUDA(cudaMemcpyAsync(out, src, n * sizeof(int32_t), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            h->c.s));
+    LV_CUDA(cudaStreamSynchronize(h->c.s));
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+louvain_status louvain_modularity(louvain_t h, int32_t level, double *q) {
+  if (!h || !q) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  if (level < -1 || level >= (int32_t)h->levels.size()) return LV_ERANGE;
+  *q = level < 0 ? h->levels.back()->q : h->levels[level]->q;
+  return LV_OK;
+}
+
+louvain_status louvain_level_stats(louvain_t h, int32_t level, int32_t *sweeps, double *times) {
+  if (!h) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  if (level < 0 || level >= (int32_t)h->levels.size()) return LV_ERANGE;
+  if (sweeps) *sweeps = h->levels[level]->sweeps;
+  if (times)
+    for (int i = 0; i < 5; ++i) times[i] = h->levels[level]->times[i];
+  return LV_OK;
+}
+
+louvain_status louvain_run_stats(louvain_t h, int64_t *edge_visits, int64_t *launches) {
+  if (!h) return LV_EINVAL;
+  if (edge_visits) *edge_visits = h->edge_visits;
+  if (launches) *launches = h->run_launches;
+  return LV_OK;
+}
+
+louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *labels_out, int32_t mode,
+                             int32_t on_device, int64_t *moved, int64_t *i2, int64_t *s2_hi, uint64_t *s2_lo) {
+  if (!h || !labels_in || !labels_out || (mode != 0 && mode != 1)) return LV_EINVAL;
+  try {
+    Ctx &c = h->c;
+    LV_CUDA(cudaSetDevice(c.device));
+    const DGraph &g = h->g0;
+    const i64 n = g.n;
+    Bins &B = vbins0(h);
+    State st;
+    st.lab[0].alloc(c.A, n);
+    st.lab[1].alloc(c.A, n);
+    st.deg.alloc(c.A, n);
+    st.size.alloc(c.A, n);
+    LV_CUDA(cudaMemcpyAsync(st.lab[0].p, labels_in, n * sizeof(int32_t),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(st.lab[1].p, st.lab[0].p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+    LV_CUDA(cudaMemsetAsync(st.deg.p, 0, n * sizeof(i64), c.s));
+    LV_CUDA(cudaMemsetAsync(st.size.p, 0, n * sizeof(int32_t), c.s));
+    Buf<int> err(c.A, 1);
+    LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
+    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg.p, st.size.p, err.p);
+    int herr = 0;
+    LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    LV_REQUIRE(herr == 0, LV_EINVAL, "labels must lie in [0,n)");
+    SweepOut o = run_pass(h, g, B, st, mode == 0 ? M_SWEEP : M_MERGE);
+    // exact Eq. 3 numerators of the snapshot (S2 over all labels, not the fused form)
+    u64 lsum;
+    u128 s2i;
+    level_consts(h, g, lsum, s2i);
+    Buf<u64> t(c.A, 2);
+    LV_CUDA(cudaMemsetAsync(t.p, 0, 2 * sizeof(u64), c.s));
+    LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, n), 256, 0, DegArr{st.deg.p}, n, t.p);
+    u64 ht[2];
+    LV_CUDA(cudaMemcpyAsync(ht, t.p, sizeof(ht), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaMemcpyAsync(labels_out, st.lab[1].p, n * sizeof(int32_t),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    if (moved) *moved = (int64_t)o.moved;
+    if (i2) *i2 = (int64_t)(o.i2 + 2 * lsum);
+    const u128 s2 = ((u128)ht[1] << 64) | ht[0];
+    if (s2_hi) *s2_hi = (int64_t)(u64)(s2 >> 64);
+    if (s2_lo) *s2_lo = (uint64_t)s2;
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char *json, int64_t cap) {
+  if (!h || !json || cap < 64 || reps < 1 || warm < 0) return LV_EINVAL;
+  try {
+    Ctx &c = h->c;
+    LV_CUDA(cudaSetDevice(c.device));
+    const DGraph &g = h->g0;
+    Bins &B = vbins0(h);
+    State st;
+    init_state(h, g, st);
+    for (int i = 0; i < warm; ++i) {
+      run_pass(h, g, B, st, M_SWEEP);
+      commit(h, g, st);
+    }
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    KTimer tm;
+    tm.on = true;
+    cudaEvent_t e0, e1;
+    LV_CUDA(cudaEventCreate(&e0));
+    LV_CUDA(cudaEventCreate(&e1));
+    double total_ms = 0;
+    std::vector<std::string> knames;
+    std::vector<double> kms, kbytes;
+    std::vector<i64> klaunch;
+    double alg_total = 0;
+    const int wb = wbytes(g.wt);
+    for (int r = 0; r < reps; ++r) {
+      tm.clear();
+      std::vector<SweepOut> pb;
+      LV_CUDA(cudaEventRecord(e0, c.s));
+      SweepOut o = run_pass(h, g, B, st, M_SWEEP, &tm, &pb);  // includes the counter D2H sync
+      tm.begin(c.s, "commit");
+      commit(h, g, st);
+      tm.end(c.s);
+      LV_CUDA(cudaEventRecord(e1, c.s));
+      LV_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      LV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      total_ms += ms;
+      // per-kernel times and algorithmic bytes
+      for (size_t k = 0; k < tm.names.size(); ++k) {
+        float kt = 0;
+        LV_CUDA(cudaEventElapsedTime(&kt, tm.ev[2 * k], tm.ev[2 * k + 1]));
+        const std::string &nm = tm.names[k];
+        double bytes = 0;
+        int bin = -1;
+        for (int b = 0; b < NSMEM; ++b)
+          if (nm == std::string("sweep:") + BIN_NAME[b]) bin = b;
+        if (bin >= 0) {
+          bytes = (double)B.edges[bin] * (8.0 + wb) + 8.0 * (double)pb[bin].cand + 48.0 * (double)B.count(bin);
+        } else if (nm == "sweep:hub_acc") {
+          bytes = (double)B.edges[NSMEM] * (8.0 + wb);
+        } else if (nm == "sweep:hub_fin") {
+          bytes = 8.0 * (double)pb[NSMEM].cand + 48.0 * (double)B.count(NSMEM);
+        } else if (nm == "commit") {
+          bytes = 8.0 * (double)g.n + 24.0 * (double)o.moved;
+        }
+        size_t j = 0;
+        while (j < knames.size() && knames[j] != nm) ++j;
+        if (j == knames.size()) {
+          knames.push_back(nm);
+          kms.push_back(0);
+          kbytes.push_back(0);
+          klaunch.push_back(0);
+        }
+        kms[j] += kt;
+        kbytes[j] += bytes;
+        klaunch[j] += 1;
+        alg_total += bytes;
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::string js = "{\"ms_sweep\": " + std::to_string(total_ms / reps) +
+                     ", \"alg_bytes_sweep\": " + std::to_string(alg_total / reps) +
+                     ", \"edges\": " + std::to_string(g.nnz) + ", \"n\": " + std::to_string(g.n) +
+                     ", \"active\": " + std::to_string(B.active()) + ", \"kernels\": [";
+    for (size_t j = 0; j < knames.size(); ++j) {
+      char buf[512];
+      snprintf(buf, sizeof(buf), "%s{\"name\": \"%s\", \"ms\": %.6f, \"alg_bytes\": %.1f, \"launches\": %lld}",
+               j ? ", " : "", knames[j].c_str(), kms[j] / reps, kbytes[j] / reps, (long long)(klaunch[j] / reps));
+      js += buf;
+    }
+    js += "]}";
+    if ((int64_t)js.size() + 1 > cap) return LV_EINVAL;
+    memcpy(json, js.c_str(), js.size() + 1);
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+louvain_status louvain_get_csr(louvain_t h, int64_t *nnz, int64_t *row_ptr, int32_t *col, int64_t *w, int64_t *loop,
+                               int64_t *delta, int64_t *W) {
+  if (!h) return LV_EINVAL;
+  try {
+    Ctx &c = h->c;
+    const DGraph &g = h->g0;
+    if (nnz) *nnz = g.nnz;
+    if (W) *W = g.W;
+    if (row_ptr) LV_CUDA(cudaMemcpyAsync(row_ptr, g.row_ptr.p, (g.n + 1) * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (col) LV_CUDA(cudaMemcpyAsync(col, g.col.p, g.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    if (loop) LV_CUDA(cudaMemcpyAsync(loop, g.loop.p, g.n * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (delta) LV_CUDA(cudaMemcpyAsync(delta, g.delta.p, g.n * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (w) {
+      Buf<i64> t(c.A, g.nnz > 0 ? g.nnz : 1);
+      if (g.wt == WT_NONE) {
+        std::vector<i64> ones(g.nnz, 1);
+        memcpy(w, ones.data(), g.nnz * sizeof(i64));
+      } else {
+        if (g.wt == WT_U32) LV_LAUNCH(c, k_to_i64<uint32_t>, grid_for(c, g.nnz), 256, 0, g.nnz, (const uint32_t *)g.w.p, t.p);
+        else LV_LAUNCH(c, k_to_i64<u64>, grid_for(c, g.nnz), 256, 0, g.nnz, (const u64 *)g.w.p, t.p);
+        LV_CUDA(cudaMemcpyAsync(w, t.p, g.nnz * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+      }
+      LV_CUDA(cudaStreamSynchronize(c.s));
+    }
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+louvain_status louvain_contract(louvain_t h, const int32_t *labels, int64_t k, int64_t *nnz_out, int64_t *row_ptr,
+                                int32_t *col, int64_t *w, int64_t *loop, int64_t *delta) {
+  if (!h || !labels || !nnz_out || k <= 0) return LV_EINVAL;
+  try {
+    Ctx &c = h->c;
+    LV_CUDA(cudaSetDevice(c.device));
+    const DGraph &g = h->g0;
+    const i64 n = g.n;
+    Buf<int32_t> lab(c.A, n);
+    LV_CUDA(cudaMemcpyAsync(lab.p, labels, n * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+    Buf<i64> ndelta(c.A, k);
+    Buf<int32_t> nsize(c.A, k);
+    LV_CUDA(cudaMemsetAsync(ndelta.p, 0, k * sizeof(i64), c.s));
+    LV_CUDA(cudaMemsetAsync(nsize.p, 0, k * sizeof(int32_t), c.s));
+    Buf<int> err(c.A, 1);
+    LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
+    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, lab.p, g.delta.p, ndelta.p, nsize.p, err.p);
+    Bins &B = vbins0(h);
+    DGraph hg;
+    contract(c, g, B, lab.p, k, std::move(ndelta), hg);
+    *nnz_out = hg.nnz;
+    if (row_ptr) LV_CUDA(cudaMemcpyAsync(row_ptr, hg.row_ptr.p, (k + 1) * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (col) LV_CUDA(cudaMemcpyAsync(col, hg.col.p, hg.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+    if (loop) LV_CUDA(cudaMemcpyAsync(loop, hg.loop.p, k * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (delta) LV_CUDA(cudaMemcpyAsync(delta, hg.delta.p, k * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    if (w) {
+      Buf<i64> t(c.A, hg.nnz > 0 ? hg.nnz : 1);
+      if (hg.wt == WT_U32) LV_LAUNCH(c, k_to_i64<uint32_t>, grid_for(c, hg.nnz), 256, 0, hg.nnz, (const uint32_t *)hg.w.p, t.p);
+      else LV_LAUNCH(c, k_to_i64<u64>, grid_for(c, hg.nnz), 256, 0, hg.nnz, (const u64 *)hg.w.p, t.p);
+      LV_CUDA(cudaMemcpyAsync(w, t.p, hg.nnz * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+      LV_CUDA(cudaStreamSynchronize(c.s));
+    }
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
+  return LV_OK;
+}
+
+const char *louvain_last_error(louvain_t h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void louvain_destroy(louvain_t h) { delete h; }
+
+// ------------------------------------------------------------------ NCCL bootstrap
+// NCCL is loaded at run time (dlopen) so the library loads on hosts without it.
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef int (*nccl_get_uid_fn)(nccl_uid_t *);
+typedef int (*nccl_init_fn)(void **, int, nccl_uid_t, int);
+typedef int (*nccl_destroy_fn)(void *);
+
+static void *nccl_lib() {
+  static void *lib = nullptr;
+  if (!lib) {
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names)
+      if ((lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  }
+  return lib;
+}
+
+louvain_status louvain_nccl_unique_id(uint8_t id[128]) {
+  void *lib = nccl_lib();
+  if (!lib || !id) return LV_ENCCL;
+  auto f = (nccl_get_uid_fn)dlsym(lib, "ncclGetUniqueId");
+  nccl_uid_t u;
+  if (!f || f(&u) != 0) return LV_ENCCL;
+  memcpy(id, u.internal, 128);
+  return LV_OK;
+}
+
+louvain_status louvain_nccl_init(const uint8_t id[128], int32_t world, int32_t rank, int32_t device, void **comm_out) {
+  void *lib = nccl_lib();
+  if (!lib || !id || !comm_out) return LV_ENCCL;
+  auto f = (nccl_init_fn)dlsym(lib, "ncclCommInitRank");
+  if (!f) return LV_ENCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return LV_ECUDA;
+  nccl_uid_t u;
+  memcpy(u.internal, id, 128);
+  return f(comm_out, world, u, rank) == 0 ? LV_OK : LV_ENCCL;
+}
+
+louvain_status louvain_nccl_destroy(void *comm) {
+  void *lib = nccl_lib();
+  if (!lib) return LV_ENCCL;
+  auto f = (nccl_destroy_fn)dlsym(lib, "ncclCommDestroy");
+  return (f && f(comm) == 0) ? LV_OK : LV_ENCCL;
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+// lv_bins.cuh — degree binning ("divergence ... could be reduced by ordering the
+// vertices by degree") and the launcher that runs one aggregation pass (sweep, merge or
+// emit) over all bins.  Bins are rebuilt once per level and reused by every sweep.
+#pragma once
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "lv_agg.cuh"
+#include "lv_scan.cuh"
+
+namespace lv {
+
+// bin b holds rows of length in (BIN_MAX[b-1], BIN_MAX[b]]; bin NSMEM holds the hubs
+constexpr int NSMEM = 8;
+constexpr int NBIN = NSMEM + 1;
+constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 8192};
+constexpr i64 HUB_CHUNK = 4096;  // edges per CTA of k_hub_acc
+
+__device__ __forceinline__ int bin_of(i64 d) {
+  if (d <= 0) return 255;
+  if (d <= 4) return 0;
+  if (d <= 8) return 1;
+  if (d <= 16) return 2;
+  if (d <= 32) return 3;
+  if (d <= 128) return 4;
+  if (d <= 512) return 5;
+  if (d <= 2048) return 6;
+  if (d <= 8192) return 7;
+  return 8;
+}
+
+struct KTimer {  // optional per-launch CUDA-event timing (louvain_time_sweeps)
+  bool on = false;
+  std::vector<std::string> names;
+  std::vector<cudaEvent_t> ev;  // pairs
+  void begin(cudaStream_t s, const std::string &n) {
+    if (!on) return;
+    cudaEvent_t a;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, s);
+    names.push_back(n);
+    ev.push_back(a);
+  }
+  void end(cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    ev.push_back(b);
+  }
+  void clear() {
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    names.clear();
+  }
+  ~KTimer() { clear(); }
+};
+
+struct Bins {
+  i64 nrows = 0;             // universe of rows considered
+  Buf<int32_t> rows;         // active rows grouped by bin (ascending id within a bin)
+  i64 off[NBIN + 1] = {0};   // host offsets of each bin in rows
+  i64 edges[NBIN] = {0};     // Σ row length per bin
+  // hub tables
+  i64 nhub = 0, nchunks = 0, tslots = 0;
+  Buf<i64> toff;
+  Buf<int32_t> tlog;
+  Buf<Chunk> chunks;
+  Buf<int32_t> tkeys;
+  Buf<u64> tvals;
+  i64 count(int b) const { return off[b + 1] - off[b]; }
+  i64 active() const { return off[NBIN]; }
+};
+
+struct LenOf {
+  const i64 *ptr;
+  __device__ __forceinline__ i64 operator()(i64 r) const { return ptr[r + 1] - ptr[r]; }
+};
+
+__global__ void k_bin_ids(i64 n, const i64 *__restrict__ ptr, uint8_t *ids) {
+  for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256)
+    ids[r] = (uint8_t)bin_of(ptr[r + 1] - ptr[r]);
+}
+
+struct BinLen {
+  const int32_t *rows;
+  const i64 *ptr;
+  __device__ __forceinline__ u64 operator()(i64 t) const { return (u64)(ptr[rows[t] + 1] - ptr[rows[t]]); }
+};
+
+struct IsBin {
+  const uint8_t *ids;
+  int b;
+  __device__ __forceinline__ i64 operator()(i64 r) const { return ids[r] == b ? 1 : 0; }
+};
+
+__global__ void k_bin_scatter(i64 n, const uint8_t *__restrict__ ids, int b, const i64 *__restrict__ pos,
+                              int32_t *out) {
+  for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256)
+    if (ids[r] == b) out[pos[r]] = (int32_t)r;
+}
+
+__global__ void k_gather_len(i64 m, const int32_t *rows, const i64 *ptr, i64 *beg, i64 *len) {
+  for (i64 t = (i64)blockIdx.x * 256 + threadIdx.x; t < m; t += (i64)gridDim.x * 256) {
+    int32_t r = rows[t];
+    beg[t] = ptr[r];
+    len[t] = ptr[r + 1] - ptr[r];
+  }
+}
+
+inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
+  i64 g = cdiv(n, per);
+  i64 cap = (i64)c.sms * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// Partition rows [0,nrows) of `ptr` into length bins; set up hub tables sized for at
+// most `universe` distinct keys per row.
+inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B) {
+  B.nrows = nrows;
+  Buf<uint8_t> ids(c.A, nrows > 0 ? nrows : 1);
+  Buf<i64> pos(c.A, nrows + 1);
+  LV_LAUNCH(c, k_bin_ids, grid_for(c, nrows), 256, 0, nrows, ptr, ids.p);
+  // counts per bin
+  std::vector<i64> cnt(NBIN, 0);
+  for (int b = 0; b < NBIN; ++b) {
+    exclusive_scan<i64>(c, IsBin{ids.p, b}, nrows, pos.p, true);
+    LV_CUDA(cudaMemcpyAsync(&cnt[b], pos.p + nrows, sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    B.off[b + 1] = B.off[b] + cnt[b];
+  }
+  B.rows.alloc(c.A, B.off[NBIN] > 0 ? B.off[NBIN] : 1);
+  for (int b = 0; b < NBIN; ++b) {
+    if (!cnt[b]) continue;
+    exclusive_scan<i64>(c, IsBin{ids.p, b}, nrows, pos.p, false);
+    LV_LAUNCH(c, k_bin_scatter, grid_for(c, nrows), 256, 0, nrows, ids.p, b, pos.p, B.rows.p + B.off[b]);
+  }
+  {
+    Buf<u64> es(c.A, NBIN);
+    LV_CUDA(cudaMemsetAsync(es.p, 0, NBIN * sizeof(u64), c.s));
+    for (int b = 0; b < NBIN; ++b)
+      if (cnt[b]) LV_LAUNCH(c, k_sum_u64<BinLen>, grid_for(c, cnt[b]), 256, 0, BinLen{B.rows.p + B.off[b], ptr}, cnt[b], es.p + b);
+    u64 he[NBIN];
+    LV_CUDA(cudaMemcpyAsync(he, es.p, NBIN * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    for (int b = 0; b < NBIN; ++b) B.edges[b] = (i64)he[b];
+  }
+  // hubs
+  B.nhub = cnt[NSMEM];
+  B.nchunks = 0;
+  B.tslots = 0;
+  if (B.nhub) {
+    Buf<i64> hb(c.A, B.nhub), hl(c.A, B.nhub);
+    LV_LAUNCH(c, k_gather_len, grid_for(c, B.nhub), 256, 0, B.nhub, B.rows.p + B.off[NSMEM], ptr, hb.p, hl.p);
+    std::vector<i64> beg(B.nhub), len(B.nhub);
+    LV_CUDA(cudaMemcpyAsync(beg.data(), hb.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaMemcpyAsync(len.data(), hl.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    std::vector<i64> toff(B.nhub);
+    std::vector<int32_t> tlog(B.nhub);
+    std::vector<Chunk> ch;
+    for (i64 h = 0; h < B.nhub; ++h) {
+      i64 want = 2 * std::min(len[h], universe);
+      int lg = 5;
+      while (((i64)1 << lg) < want) ++lg;
+      tlog[h] = lg;
+      toff[h] = B.tslots;
+      B.tslots += (i64)1 << lg;
+      for (i64 e = 0; e < len[h]; e += HUB_CHUNK) {
+        Chunk k;
+        k.beg = beg[h] + e;
+        k.end = beg[h] + std::min(len[h], e + HUB_CHUNK);
+        k.h = (int32_t)h;
+        k.pad = 0;
+        ch.push_back(k);
+      }
+    }
+    B.nchunks = (i64)ch.size();
+    B.toff.alloc(c.A, B.nhub);
+    B.tlog.alloc(c.A, B.nhub);
+    B.chunks.alloc(c.A, B.nchunks);
+    B.tkeys.alloc(c.A, B.tslots);
+    B.tvals.alloc(c.A, B.tslots);
+    LV_CUDA(cudaMemcpyAsync(B.toff.p, toff.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.tlog.p, tlog.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.chunks.p, ch.data(), B.nchunks * sizeof(Chunk), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemsetAsync(B.tkeys.p, 0xff, B.tslots * sizeof(int32_t), c.s));
+    LV_CUDA(cudaMemsetAsync(B.tvals.p, 0, B.tslots * sizeof(u64), c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));  // host vectors go out of scope
+  }
+}
+
+// ----------------------------------------------------------------- launch
+template <int G, int CAP, int BLOCK, int MODE, class WT>
+void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
+  auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT>;
+  constexpr int GPB = BLOCK / G;
+  const size_t smem = (size_t)GPB * CAP * (sizeof(u64) + sizeof(int32_t));
+  static int occ = -1;
+  if (occ < 0) {
+    if (smem > 48 * 1024) LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int o = 0;
+    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, smem));
+    occ = o > 0 ? o : 1;
+  }
+  i64 grid = cdiv(a.nrows, GPB);
+  i64 cap = (i64)c.sms * occ * 8;
+  if (grid > cap) grid = cap;
+  if (tm) tm->begin(c.s, tag);
+  LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, smem, a);
+  if (tm) tm->end(c.s);
+}
+
+static const char *BIN_NAME[NBIN] = {"agg_g4_c8",      "agg_g8_c16",      "agg_g16_c32",
+                                     "agg_g32_c64",    "agg_g32_c256",    "agg_blk128_c1024",
+                                     "agg_blk256_c4096", "agg_blk512_c16384", "agg_hub"};
+
+// One pass of MODE over every bin of B.  `a` carries the common arguments.
+template <int MODE, class WT>
+void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
+  static const char *MN[3] = {"sweep", "merge", "emit"};
+  u64 *ctr = a.counters;  // NBIN slots of 8 counters (one per bin) or NULL
+  auto set = [&](int b) {
+    a.rows = B.rows.p + B.off[b];
+    a.nrows = B.count(b);
+    a.counters = ctr ? ctr + 8 * b : nullptr;
+  };
+  std::string pre = std::string(MN[MODE]) + ":";
+  // hub path first (longest rows), then the big bins, then the small ones
+  if (B.nhub) {
+    set(NSMEM);
+    a.tkeys = B.tkeys.p;
+    a.tvals = B.tvals.p;
+    a.toff = B.toff.p;
+    a.tlog = B.tlog.p;
+    a.chunks = B.chunks.p;
+    if (tm) tm->begin(c.s, pre + "hub_acc");
+    LV_LAUNCH(c, (k_hub_acc<MODE, WT>), (unsigned)B.nchunks, HUB_ACC_T, 0, a);
+    if (tm) tm->end(c.s);
+    if (tm) tm->begin(c.s, pre + "hub_fin");
+    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nhub, HUB_FIN_T, 0, a);
+    if (tm) tm->end(c.s);
+  }
+  if (B.count(7)) { set(7); launch_bin<512, 16384, 512, MODE, WT>(c, tm, a, (pre + BIN_NAME[7]).c_str()); }
+  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[6]).c_str()); }
+  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT>(c, tm, a, (pre + BIN_NAME[5]).c_str()); }
+  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[4]).c_str()); }
+  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[3]).c_str()); }
+  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[2]).c_str()); }
+  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[1]).c_str()); }
+  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[0]).c_str()); }
+}
+
+template <int MODE>
+void launch_agg_wt(Ctx &c, int wt, const Bins &B, const AggArgs &a, KTimer *tm = nullptr) {
+  if (wt == WT_NONE) launch_agg<MODE, WNone>(c, B, a, tm);
+  else if (wt == WT_U32) launch_agg<MODE, WU32>(c, B, a, tm);
+  else launch_agg<MODE, WU64>(c, B, a, tm);
+}
+
+}  // namespace lv

@@ -1,0 +1,162 @@
+// lv_common.cuh — shared plumbing of liblouvain (sm_100a): error handling, the device
+// allocator, launch accounting and small device helpers (warp/block reductions).
+// Nothing here implements a step of the method; see lv_agg.cuh / lv_graph.cuh.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "louvain.h"
+
+namespace lv {
+
+typedef unsigned long long u64;
+typedef long long i64;
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define LV_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::lv::Error{LV_ECUDA, std::string(#x) + " -> " + cudaGetErrorString(e_) +       \
+                                      " @" + __FILE__ + ":" + std::to_string(__LINE__)};    \
+  } while (0)
+
+#define LV_REQUIRE(cond, code, msg)                      \
+  do {                                                   \
+    if (!(cond)) throw ::lv::Error{(code), (msg)};      \
+  } while (0)
+
+// ------------------------------------------------------------------ device memory
+struct Alloc {
+  louvain_alloc_fn a = nullptr;
+  louvain_free_fn f = nullptr;
+  void *ctx = nullptr;
+  cudaStream_t s = nullptr;
+  size_t live = 0, peak = 0;
+
+  void *get(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    void *p = nullptr;
+    if (a) {
+      p = a(ctx, bytes, (void *)s);
+      LV_REQUIRE(p != nullptr, LV_ENOMEM, "device allocation hook failed (" + std::to_string(bytes) + " B)");
+    } else {
+      cudaError_t e = cudaMallocAsync(&p, bytes, s);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{LV_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e)};
+      }
+    }
+    live += bytes;
+    if (live > peak) peak = live;
+    return p;
+  }
+  void put(void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    live -= bytes;
+    if (f) f(ctx, p, bytes, (void *)s);
+    else cudaFreeAsync(p, s);
+  }
+};
+
+// RAII device buffer (stream-ordered).
+template <typename T>
+struct Buf {
+  T *p = nullptr;
+  size_t n = 0;
+  Alloc *A = nullptr;
+  Buf() {}
+  Buf(Alloc &al, size_t count) { alloc(al, count); }
+  void alloc(Alloc &al, size_t count) {
+    release();
+    A = &al;
+    n = count;
+    p = (T *)al.get(count * sizeof(T));
+  }
+  void release() {
+    if (p && A) A->put(p, n * sizeof(T));
+    p = nullptr;
+    n = 0;
+  }
+  ~Buf() { release(); }
+  Buf(const Buf &) = delete;
+  Buf &operator=(const Buf &) = delete;
+  Buf(Buf &&o) noexcept : p(o.p), n(o.n), A(o.A) { o.p = nullptr; o.n = 0; }
+  Buf &operator=(Buf &&o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; A = o.A;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  T *get() const { return p; }
+};
+
+// Execution context: device, stream, allocator, launch accounting.
+struct Ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t s = nullptr;
+  Alloc A;
+  i64 launches = 0;
+};
+
+#define LV_LAUNCH(ctx, kern, grid, block, smem, ...)                          \
+  do {                                                                        \
+    kern<<<(grid), (block), (smem), (ctx).s>>>(__VA_ARGS__);                  \
+    (ctx).launches++;                                                         \
+    LV_CUDA(cudaGetLastError());                                              \
+  } while (0)
+
+inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ u64 warp_sum_u64(u64 v, unsigned mask = 0xffffffffu) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+// exact 128-bit add of (hi,lo) pairs
+__device__ __forceinline__ void add128(u64 &hi, u64 &lo, u64 ohi, u64 olo) {
+  u64 nlo = lo + olo;
+  hi = hi + ohi + (nlo < lo ? 1ull : 0ull);
+  lo = nlo;
+}
+
+// Atomically add a 128-bit unsigned value (hi,lo) into two u64 words (order-free exact).
+__device__ __forceinline__ void atomic_add128(u64 *dst_lo, u64 *dst_hi, u64 hi, u64 lo) {
+  u64 old = atomicAdd(dst_lo, lo);
+  u64 carry = (old + lo < old) ? 1ull : 0ull;
+  if (hi + carry) atomicAdd(dst_hi, hi + carry);
+}
+
+// Block-wide sum of a u64 (all threads call; result valid in every thread).
+template <int BLOCK>
+__device__ __forceinline__ u64 block_sum_u64(u64 v) {
+  __shared__ u64 red[BLOCK / 32];
+  v = warp_sum_u64(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  u64 t = 0;
+#pragma unroll
+  for (int i = 0; i < BLOCK / 32; ++i) t += red[i];
+  return t;
+}
+
+}  // namespace lv

@@ -1,0 +1,427 @@
+// lv_graph.cuh — device graph (CSR) construction, renumbering and contraction.
+//
+//   build_csr  : §5.1.2 "Neighbor computation": loops to loop[] (reading
+//                D2), mirror every non-loop record, group by source (counting pass +
+//                prefix sum instead of the paper's sort_by_key), merge duplicates with the
+//                hash aggregation (instead of reduce_by_key, reading D25), offsets by
+//                exclusive scan, δ_i = Σ_j ω(i,j) + 2·loop_i, W = Σ ω.
+//   renumber   : "Renumbering nodes": flag non-empty labels, exclusive scan,
+//                order-preserving dense ids (reading D18).
+//   contract   : "Inducing new graph" / graph rebuilding: rows of
+//                each community's members are gathered into one contiguous range with
+//                their neighbours' new ids, then hash-aggregated (instead of sort_by_key +
+//                reduce_by_key): inter-community weights summed per pair, intra weight to
+//                the meta-vertex loop (old loops once; reading D19); δ' = deg_C, W' = W.
+#pragma once
+#include <cstring>
+
+#include "lv_bins.cuh"
+
+namespace lv {
+
+struct DGraph {
+  i64 n = 0, nnz = 0, W = 0;
+  int wt = WT_NONE;
+  Buf<i64> row_ptr;       // n+1
+  Buf<int32_t> col;       // nnz
+  Buf<unsigned char> w;   // nnz * wbytes(wt)
+  Buf<i64> loop, delta;   // n
+};
+
+inline int wbytes(int wt) { return wt == WT_NONE ? 0 : wt == WT_U32 ? 4 : 8; }
+
+// ------------------------------------------------------------------ COO -> CSR
+struct RNone { __device__ __forceinline__ static i64 get(const void *, i64) { return 1; } };
+struct RI32 { __device__ __forceinline__ static i64 get(const void *w, i64 k) { return ((const int32_t *)w)[k]; } };
+struct RI64 { __device__ __forceinline__ static i64 get(const void *w, i64 k) { return ((const i64 *)w)[k]; } };
+
+template <class R>
+__global__ void __launch_bounds__(256) k_coo_count(i64 m, i64 n, const int32_t *__restrict__ src,
+                                                   const int32_t *__restrict__ dst, const void *w, i64 *loop,
+                                                   uint32_t *cnt, u64 *Wacc, int *err) {
+  u64 s = 0;
+  for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
+    const int32_t u = src[k], v = dst[k];
+    const i64 wk = R::get(w, k);
+    if (u < 0 || v < 0 || u >= n || v >= n || wk <= 0) {
+      atomicOr(err, 1);
+      continue;
+    }
+    s += (u64)wk;
+    if (u == v) {
+      atomicAdd((u64 *)&loop[u], (u64)wk);
+    } else {
+      atomicAdd(&cnt[u], 1u);
+      atomicAdd(&cnt[v], 1u);
+    }
+  }
+  s = block_sum_u64<256>(s);
+  if (threadIdx.x == 0 && s) atomicAdd(Wacc, s);
+}
+
+template <class R, class WOUT>
+__global__ void __launch_bounds__(256) k_coo_fill(i64 m, const int32_t *__restrict__ src,
+                                                  const int32_t *__restrict__ dst, const void *w,
+                                                  const i64 *__restrict__ rptr, uint32_t *cur, int32_t *rcol,
+                                                  void *rw) {
+  for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
+    const int32_t u = src[k], v = dst[k];
+    if (u == v) continue;
+    const i64 wk = R::get(w, k);
+    i64 pu = rptr[u] + atomicAdd(&cur[u], 1u);
+    i64 pv = rptr[v] + atomicAdd(&cur[v], 1u);
+    rcol[pu] = v;
+    rcol[pv] = u;
+    if (WOUT::bytes == 4) { ((uint32_t *)rw)[pu] = (uint32_t)wk; ((uint32_t *)rw)[pv] = (uint32_t)wk; }
+    if (WOUT::bytes == 8) { ((u64 *)rw)[pu] = (u64)wk; ((u64 *)rw)[pv] = (u64)wk; }
+  }
+}
+
+// Copy each row's first cnt[r] entries (keys + u64 weights) from src_base[r] to
+// dst_ptr[r], converting the weight to WOUT.  One group of G lanes per row.
+template <int G, int BLOCK, class WOUT>
+__global__ void __launch_bounds__(BLOCK) k_copy_rows(const int32_t *__restrict__ rows, i64 nrows,
+                                                     const i64 *__restrict__ src_base, const i64 *__restrict__ cnt,
+                                                     const i64 *__restrict__ dst_ptr, const int32_t *__restrict__ skey,
+                                                     const u64 *__restrict__ sw, int32_t *dkey, void *dw) {
+  constexpr int GPB = BLOCK / G;
+  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+  for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < nrows; idx += (i64)gridDim.x * GPB) {
+    const int32_t r = rows[idx];
+    const i64 s = src_base[r], d = dst_ptr[r], c = cnt[r];
+    for (i64 t = lane; t < c; t += G) {
+      dkey[d + t] = skey[s + t];
+      if (WOUT::bytes == 4) ((uint32_t *)dw)[d + t] = (uint32_t)sw[s + t];
+      if (WOUT::bytes == 8) ((u64 *)dw)[d + t] = sw[s + t];
+    }
+  }
+}
+
+// Hub rows: chunked copy (chunks cover the row's source range; copy the part < cnt).
+template <class WOUT>
+__global__ void __launch_bounds__(256) k_copy_hub(const Chunk *__restrict__ chunks, const int32_t *__restrict__ rows,
+                                                  const i64 *__restrict__ src_base, const i64 *__restrict__ cnt,
+                                                  const i64 *__restrict__ dst_ptr, const int32_t *__restrict__ skey,
+                                                  const u64 *__restrict__ sw, int32_t *dkey, void *dw) {
+  const Chunk ch = chunks[blockIdx.x];
+  const int32_t r = rows[ch.h];
+  const i64 s = src_base[r], d = dst_ptr[r], c = cnt[r];
+  const i64 t0 = ch.beg - s, t1 = min(ch.end - s, c);
+  for (i64 t = t0 + threadIdx.x; t < t1; t += 256) {
+    dkey[d + t] = skey[s + t];
+    if (WOUT::bytes == 4) ((uint32_t *)dw)[d + t] = (uint32_t)sw[s + t];
+    if (WOUT::bytes == 8) ((u64 *)dw)[d + t] = sw[s + t];
+  }
+}
+
+template <class WOUT>
+void copy_rows_t(Ctx &c, const Bins &B, const i64 *src_base, const i64 *cnt, const i64 *dst_ptr,
+                 const int32_t *skey, const u64 *sw, int32_t *dkey, void *dw) {
+  auto one = [&](int b, auto kern, int GPB, int BLOCK) {
+    if (!B.count(b)) return;
+    i64 grid = cdiv(B.count(b), GPB);
+    if (grid > (i64)c.sms * 16) grid = (i64)c.sms * 16;
+    LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, 0, B.rows.p + B.off[b], B.count(b), src_base, cnt, dst_ptr, skey, sw,
+              dkey, dw);
+  };
+  one(0, k_copy_rows<4, 256, WOUT>, 64, 256);
+  one(1, k_copy_rows<8, 256, WOUT>, 32, 256);
+  one(2, k_copy_rows<16, 256, WOUT>, 16, 256);
+  one(3, k_copy_rows<32, 256, WOUT>, 8, 256);
+  one(4, k_copy_rows<32, 256, WOUT>, 8, 256);
+  one(5, k_copy_rows<128, 256, WOUT>, 2, 256);
+  one(6, k_copy_rows<256, 256, WOUT>, 1, 256);
+  one(7, k_copy_rows<256, 256, WOUT>, 1, 256);
+  if (B.nhub)
+    LV_LAUNCH(c, k_copy_hub<WOUT>, (unsigned)B.nchunks, 256, 0, B.chunks.p, B.rows.p + B.off[NSMEM], src_base, cnt,
+              dst_ptr, skey, sw, dkey, dw);
+}
+
+inline void copy_rows(Ctx &c, int wt, const Bins &B, const i64 *src_base, const i64 *cnt, const i64 *dst_ptr,
+                      const int32_t *skey, const u64 *sw, int32_t *dkey, void *dw) {
+  if (wt == WT_NONE) copy_rows_t<WNone>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
+  else if (wt == WT_U32) copy_rows_t<WU32>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
+  else copy_rows_t<WU64>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
+}
+
+__global__ void k_delta(i64 n, const u64 *__restrict__ rowsum, const i64 *__restrict__ loop, i64 *delta) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256)
+    delta[i] = (i64)rowsum[i] + 2 * loop[i];
+}
+
+struct U32AsI64 {
+  const uint32_t *a;
+  __device__ __forceinline__ i64 operator()(i64 i) const { return (i64)a[i]; }
+};
+struct I64Arr {
+  const i64 *a;
+  __device__ __forceinline__ i64 operator()(i64 i) const { return a[i]; }
+};
+
+inline i64 d2h_i64(Ctx &c, const i64 *p) {
+  i64 v;
+  LV_CUDA(cudaMemcpyAsync(&v, p, sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  return v;
+}
+
+// Build the level-0 CSR from device COO records.  Returns LV_OK / LV_EGRAPH / LV_EZEROW
+// through exceptions.  in_wt: 0 none, 1 int32, 2 int64 (louvain_wtype).
+inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *dst, const void *w, int in_wt,
+                      DGraph &g) {
+  g.n = n;
+  g.loop.alloc(c.A, n);
+  g.delta.alloc(c.A, n);
+  LV_CUDA(cudaMemsetAsync(g.loop.p, 0, n * sizeof(i64), c.s));
+  Buf<uint32_t> cnt(c.A, n);
+  LV_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(uint32_t), c.s));
+  Buf<u64> scal(c.A, 2);  // [0] W, [1] err
+  LV_CUDA(cudaMemsetAsync(scal.p, 0, 2 * sizeof(u64), c.s));
+  int *err = (int *)(scal.p + 1);
+  const unsigned gm = grid_for(c, m);
+  if (m > 0) {
+    if (in_wt == LV_W_NONE) LV_LAUNCH(c, k_coo_count<RNone>, gm, 256, 0, m, n, src, dst, w, g.loop.p, cnt.p, scal.p, err);
+    else if (in_wt == LV_W_I32) LV_LAUNCH(c, k_coo_count<RI32>, gm, 256, 0, m, n, src, dst, w, g.loop.p, cnt.p, scal.p, err);
+    else LV_LAUNCH(c, k_coo_count<RI64>, gm, 256, 0, m, n, src, dst, w, g.loop.p, cnt.p, scal.p, err);
+  }
+  u64 hs[2];
+  LV_CUDA(cudaMemcpyAsync(hs, scal.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  LV_REQUIRE(((int)hs[1]) == 0, LV_EGRAPH, "vertex id outside [0,n) or weight <= 0 (P:L43: positive weights)");
+  g.W = (i64)hs[0];
+  LV_REQUIRE(g.W > 0, LV_EZEROW, "W = 0: modularity (Eq. 3) is undefined");
+  // raw (duplicated) adjacency
+  Buf<i64> rptr(c.A, n + 1);
+  exclusive_scan<i64>(c, U32AsI64{cnt.p}, n, rptr.p, true);
+  const i64 rnnz = d2h_i64(c, rptr.p + n);
+  const int raw_wt = in_wt == LV_W_NONE ? WT_NONE : in_wt == LV_W_I32 ? WT_U32 : WT_U64;
+  Buf<int32_t> rcol(c.A, rnnz > 0 ? rnnz : 1);
+  Buf<unsigned char> rw(c.A, rnnz * (i64)wbytes(raw_wt) + 8);
+  LV_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(uint32_t), c.s));
+  if (m > 0) {
+    if (in_wt == LV_W_NONE) LV_LAUNCH(c, (k_coo_fill<RNone, WNone>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
+    else if (in_wt == LV_W_I32) LV_LAUNCH(c, (k_coo_fill<RI32, WU32>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
+    else LV_LAUNCH(c, (k_coo_fill<RI64, WU64>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
+  }
+  cnt.release();
+  // merge duplicates per row (hash aggregation, emit mode)
+  Bins B;
+  build_bins(c, rptr.p, n, n, B);
+  Buf<int32_t> tk(c.A, rnnz > 0 ? rnnz : 1);
+  Buf<u64> tw(c.A, rnnz > 0 ? rnnz : 1);
+  Buf<i64> ocnt(c.A, n);
+  Buf<u64> osum(c.A, n);
+  LV_CUDA(cudaMemsetAsync(ocnt.p, 0, n * sizeof(i64), c.s));
+  LV_CUDA(cudaMemsetAsync(osum.p, 0, n * sizeof(u64), c.s));
+  AggArgs a;
+  memset(&a, 0, sizeof(a));
+  a.ptr = rptr.p;
+  a.keys = rcol.p;
+  a.w = rw.p;
+  a.out_key = tk.p;
+  a.out_w = tw.p;
+  a.out_cnt = ocnt.p;
+  a.out_sum = osum.p;
+  launch_agg_wt<M_EMIT>(c, raw_wt, B, a);
+  rcol.release();
+  rw.release();
+  g.row_ptr.alloc(c.A, n + 1);
+  exclusive_scan<i64>(c, I64Arr{ocnt.p}, n, g.row_ptr.p, true);
+  g.nnz = d2h_i64(c, g.row_ptr.p + n);
+  if (raw_wt == WT_NONE && g.nnz == rnnz) g.wt = WT_NONE;
+  else g.wt = (g.W < ((i64)1 << 32)) ? WT_U32 : WT_U64;
+  g.col.alloc(c.A, g.nnz > 0 ? g.nnz : 1);
+  g.w.alloc(c.A, g.nnz * (i64)wbytes(g.wt) + 8);
+  copy_rows(c, g.wt, B, rptr.p, ocnt.p, g.row_ptr.p, tk.p, tw.p, g.col.p, g.w.p);
+  LV_LAUNCH(c, k_delta, grid_for(c, n), 256, 0, n, osum.p, g.loop.p, g.delta.p);
+  LV_CUDA(cudaStreamSynchronize(c.s));
+}
+
+// ------------------------------------------------------------------ renumber
+struct NonEmpty {
+  const int32_t *size;
+  __device__ __forceinline__ i64 operator()(i64 c) const { return size[c] > 0 ? 1 : 0; }
+};
+
+__global__ void k_apply_newid(i64 n, const i64 *__restrict__ newid, const int32_t *__restrict__ lab_in, int32_t *lab_out) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256)
+    lab_out[i] = (int32_t)newid[lab_in[i]];
+}
+
+__global__ void k_newcomm(i64 n, const i64 *__restrict__ newid, const int32_t *__restrict__ size,
+                          const i64 *__restrict__ deg, i64 *ndelta) {
+  for (i64 c = (i64)blockIdx.x * 256 + threadIdx.x; c < n; c += (i64)gridDim.x * 256)
+    if (size[c] > 0) ndelta[newid[c]] = deg[c];
+}
+
+// Order-preserving renumbering (D18): lab_out[i] = rank of lab_in[i] among non-empty
+// labels.  Returns k; ndelta (allocated here, length k) receives deg of each community.
+inline i64 renumber(Ctx &c, i64 n, const int32_t *lab_in, const int32_t *size, const i64 *deg, int32_t *lab_out,
+                    Buf<i64> &ndelta) {
+  Buf<i64> newid(c.A, n + 1);
+  exclusive_scan<i64>(c, NonEmpty{size}, n, newid.p, true);
+  const i64 k = d2h_i64(c, newid.p + n);
+  LV_LAUNCH(c, k_apply_newid, grid_for(c, n), 256, 0, n, newid.p, lab_in, lab_out);
+  ndelta.alloc(c.A, k > 0 ? k : 1);
+  LV_LAUNCH(c, k_newcomm, grid_for(c, n), 256, 0, n, newid.p, size, deg, ndelta.p);
+  return k;
+}
+
+// ------------------------------------------------------------------ contraction
+__global__ void k_comm_edges(i64 n, const int32_t *__restrict__ lab, const i64 *__restrict__ rp,
+                             const i64 *__restrict__ loop, i64 *ecnt, i64 *nloop) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    const int32_t c = lab[i];
+    const i64 d = rp[i + 1] - rp[i];
+    if (d) atomicAdd((u64 *)&ecnt[c], (u64)d);
+    if (loop[i]) atomicAdd((u64 *)&nloop[c], (u64)loop[i]);
+  }
+}
+
+// Gather each vertex's row into its community's contiguous range, mapping neighbours
+// to their new ids.  One group of G lanes per vertex (vertex bins of the level graph).
+template <int G, int BLOCK, class WT>
+__global__ void __launch_bounds__(BLOCK) k_permute(const int32_t *__restrict__ rows, i64 nrows,
+                                                   const i64 *__restrict__ rp, const int32_t *__restrict__ col,
+                                                   const void *w, const int32_t *__restrict__ lab,
+                                                   const i64 *__restrict__ cptr, u64 *ecur, int32_t *pk, void *pw) {
+  constexpr int GPB = BLOCK / G;
+  __shared__ i64 sbase[GPB];
+  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+  const unsigned mask = G >= 32 ? 0xffffffffu : (((1u << (G & 31)) - 1u) << (((threadIdx.x & 31) / G) * G));
+  for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < nrows; idx += (i64)gridDim.x * GPB) {
+    const int32_t v = rows[idx];
+    const i64 b = rp[v], d = rp[v + 1] - b;
+    const int32_t c = lab[v];
+    i64 base = 0;
+    if (lane == 0) base = cptr[c] + (i64)atomicAdd(&ecur[c], (u64)d);
+    if (G <= 32) {
+      base = __shfl_sync(mask, base, 0, G < 32 ? G : 32);
+    } else {
+      if (lane == 0) sbase[grp] = base;
+      __syncthreads();
+      base = sbase[grp];
+    }
+    for (i64 t = lane; t < d; t += G) {
+      pk[base + t] = lab[col[b + t]];
+      if (WT::bytes == 4) ((uint32_t *)pw)[base + t] = ((const uint32_t *)w)[b + t];
+      if (WT::bytes == 8) ((u64 *)pw)[base + t] = ((const u64 *)w)[b + t];
+    }
+    if (G > 32) __syncthreads();
+  }
+}
+
+template <class WT>
+__global__ void __launch_bounds__(256) k_permute_hub(const Chunk *__restrict__ chunks, const int32_t *__restrict__ rows,
+                                                     const i64 *__restrict__ rp, const int32_t *__restrict__ col,
+                                                     const void *w, const int32_t *__restrict__ lab,
+                                                     const i64 *__restrict__ hub_base, int32_t *pk, void *pw) {
+  const Chunk ch = chunks[blockIdx.x];
+  const int32_t v = rows[ch.h];
+  const i64 b = rp[v], base = hub_base[ch.h];
+  for (i64 e = ch.beg + threadIdx.x; e < ch.end; e += 256) {
+    const i64 t = e - b;
+    pk[base + t] = lab[col[e]];
+    if (WT::bytes == 4) ((uint32_t *)pw)[base + t] = ((const uint32_t *)w)[e];
+    if (WT::bytes == 8) ((u64 *)pw)[base + t] = ((const u64 *)w)[e];
+  }
+}
+
+__global__ void k_hub_bases(i64 nhub, const int32_t *__restrict__ rows, const i64 *__restrict__ rp,
+                            const int32_t *__restrict__ lab, const i64 *__restrict__ cptr, u64 *ecur, i64 *hub_base) {
+  for (i64 h = (i64)blockIdx.x * 256 + threadIdx.x; h < nhub; h += (i64)gridDim.x * 256) {
+    const int32_t v = rows[h];
+    const i64 d = rp[v + 1] - rp[v];
+    const int32_t c = lab[v];
+    hub_base[h] = cptr[c] + (i64)atomicAdd(&ecur[c], (u64)d);
+  }
+}
+
+template <class WT>
+void permute_t(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, const i64 *cptr, u64 *ecur, int32_t *pk,
+               void *pw) {
+  auto one = [&](int b, auto kern, int GPB, int BLOCK) {
+    if (!VB.count(b)) return;
+    i64 grid = cdiv(VB.count(b), GPB);
+    if (grid > (i64)c.sms * 16) grid = (i64)c.sms * 16;
+    LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, 0, VB.rows.p + VB.off[b], VB.count(b), g.row_ptr.p, g.col.p,
+              (const void *)g.w.p, lab, cptr, ecur, pk, pw);
+  };
+  one(0, k_permute<4, 256, WT>, 64, 256);
+  one(1, k_permute<8, 256, WT>, 32, 256);
+  one(2, k_permute<16, 256, WT>, 16, 256);
+  one(3, k_permute<32, 256, WT>, 8, 256);
+  one(4, k_permute<32, 256, WT>, 8, 256);
+  one(5, k_permute<128, 128, WT>, 1, 128);
+  one(6, k_permute<256, 256, WT>, 1, 256);
+  one(7, k_permute<256, 256, WT>, 1, 256);
+  if (VB.nhub) {
+    Buf<i64> hb(c.A, VB.nhub);
+    LV_LAUNCH(c, k_hub_bases, grid_for(c, VB.nhub), 256, 0, VB.nhub, VB.rows.p + VB.off[NSMEM], g.row_ptr.p, lab,
+              cptr, ecur, hb.p);
+    LV_LAUNCH(c, k_permute_hub<WT>, (unsigned)VB.nchunks, 256, 0, VB.chunks.p, VB.rows.p + VB.off[NSMEM], g.row_ptr.p,
+              g.col.p, (const void *)g.w.p, lab, hb.p, pk, pw);
+  }
+}
+
+__global__ void k_finish_loop(i64 k, const i64 *__restrict__ nloop, const u64 *__restrict__ selfw, i64 *loop_out) {
+  for (i64 c = (i64)blockIdx.x * 256 + threadIdx.x; c < k; c += (i64)gridDim.x * 256)
+    loop_out[c] = nloop[c] + (i64)(selfw[c] / 2);  // each undirected intra edge seen twice
+}
+
+// Contract g by dense labels lab (values in [0,k)); ndelta = deg of each community.
+// VB = vertex bins of g (reused from the sweeps).
+inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, i64 k, Buf<i64> &&ndelta,
+                     DGraph &h) {
+  const i64 n = g.n;
+  Buf<i64> ecnt(c.A, k + 1), nloop(c.A, k);
+  LV_CUDA(cudaMemsetAsync(ecnt.p, 0, (k + 1) * sizeof(i64), c.s));
+  LV_CUDA(cudaMemsetAsync(nloop.p, 0, k * sizeof(i64), c.s));
+  LV_LAUNCH(c, k_comm_edges, grid_for(c, n), 256, 0, n, lab, g.row_ptr.p, g.loop.p, ecnt.p, nloop.p);
+  Buf<i64> cptr(c.A, k + 1);
+  exclusive_scan<i64>(c, I64Arr{ecnt.p}, k, cptr.p, true);
+  const i64 tot = g.nnz;
+  Buf<int32_t> pk(c.A, tot > 0 ? tot : 1);
+  Buf<unsigned char> pw(c.A, tot * (i64)wbytes(g.wt) + 8);
+  LV_CUDA(cudaMemsetAsync(ecnt.p, 0, (k + 1) * sizeof(i64), c.s));  // reuse as cursor
+  if (g.wt == WT_NONE) permute_t<WNone>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
+  else if (g.wt == WT_U32) permute_t<WU32>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
+  else permute_t<WU64>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
+  ecnt.release();
+  // aggregate each community's range
+  Bins CB;
+  build_bins(c, cptr.p, k, k, CB);
+  Buf<int32_t> tk(c.A, tot > 0 ? tot : 1);
+  Buf<u64> tw(c.A, tot > 0 ? tot : 1);
+  Buf<i64> ocnt(c.A, k);
+  Buf<u64> oself(c.A, k);
+  LV_CUDA(cudaMemsetAsync(ocnt.p, 0, k * sizeof(i64), c.s));
+  LV_CUDA(cudaMemsetAsync(oself.p, 0, k * sizeof(u64), c.s));
+  AggArgs a;
+  memset(&a, 0, sizeof(a));
+  a.ptr = cptr.p;
+  a.keys = pk.p;
+  a.w = pw.p;
+  a.out_key = tk.p;
+  a.out_w = tw.p;
+  a.out_cnt = ocnt.p;
+  a.out_self = oself.p;
+  launch_agg_wt<M_EMIT>(c, g.wt, CB, a);
+  pk.release();
+  pw.release();
+  h.n = k;
+  h.W = g.W;
+  h.row_ptr.alloc(c.A, k + 1);
+  exclusive_scan<i64>(c, I64Arr{ocnt.p}, k, h.row_ptr.p, true);
+  h.nnz = d2h_i64(c, h.row_ptr.p + k);
+  h.wt = (g.W < ((i64)1 << 32)) ? WT_U32 : WT_U64;
+  h.col.alloc(c.A, h.nnz > 0 ? h.nnz : 1);
+  h.w.alloc(c.A, h.nnz * (i64)wbytes(h.wt) + 8);
+  copy_rows(c, h.wt, CB, cptr.p, ocnt.p, h.row_ptr.p, tk.p, tw.p, h.col.p, h.w.p);
+  h.loop.alloc(c.A, k);
+  LV_LAUNCH(c, k_finish_loop, grid_for(c, k), 256, 0, k, nloop.p, oself.p, h.loop.p);
+  h.delta = std::move(ndelta);
+  LV_CUDA(cudaStreamSynchronize(c.s));
+}
+
+}  // namespace lv

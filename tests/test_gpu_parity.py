@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit for bit.
+
+Integer-weighted inputs make every label a mathematical function of the input, so the
+bar is exact equality of labels, CSR arrays, Eq. 3 numerators and Q (north_star: labels
+bit-exact per level, Q within 1e-9 relative — equality is stronger).  Inputs are seeded
+synthetic graphs from paper_1805_10904_b200.inputs.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1805_10904_b200 import Louvain, LouvainError, inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _canon(rp, col, w):
+    """Rows sorted by column (row order within a row is not specified by the method)."""
+    col2, w2 = col.copy(), w.copy()
+    for i in range(len(rp) - 1):
+        s = slice(rp[i], rp[i + 1])
+        o = np.argsort(col[s], kind="stable")
+        col2[s] = col[s][o]
+        w2[s] = w[s][o]
+    return col2, w2
+
+
+def _canon_fast(rp, col, w):
+    n = len(rp) - 1
+    row = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    o = np.lexsort((col, row))
+    return col[o], w[o]
+
+
+def _random_records(seed, n, m, loops=True, wmax=5):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m, dtype=np.int64).astype(np.int32)
+    dst = rng.integers(0, n, m, dtype=np.int64).astype(np.int32)
+    if not loops:
+        keep = src != dst
+        src, dst = src[keep], dst[keep]
+    w = rng.integers(1, wmax + 1, len(src)).astype(np.int64)
+    return inputs.Records(n, src, dst, w, name=f"random({seed})")
+
+
+def _star_plus(seed=0, hub_deg=20000):
+    """A graph with rows in every degree bin incl. the hub path (> 8192)."""
+    rng = np.random.default_rng(seed)
+    n = 40000
+    src, dst = [], []
+    src += [0] * hub_deg
+    dst += list(rng.choice(np.arange(1, n), hub_deg, replace=False))
+    for d, cnt in ((3, 2000), (7, 1000), (15, 500), (30, 300), (100, 100), (400, 30), (1500, 10), (6000, 3)):
+        for _ in range(cnt):
+            v = int(rng.integers(1, n))
+            nb = rng.integers(0, n, d)
+            src += [v] * d
+            dst += list(nb)
+    src, dst = np.array(src, np.int32), np.array(dst, np.int32)
+    w = rng.integers(1, 4, len(src)).astype(np.int32)
+    return inputs.Records(n, src, dst, w, name="star_plus")
+
+
+GRAPHS = {
+    "karate": lambda: inputs.karate(),
+    "ring": lambda: inputs.ring_of_cliques(10, 6),
+    "random_loops_dups": lambda: _random_records(1, 500, 4000),
+    "rmat12": lambda: inputs.rmat(12, 16, seed=4),
+    "sbm": lambda: inputs.sbm(20_000, 20, 32, 0.3, seed=2),
+    "cooc": lambda: inputs.cooc(topics=40, topic_size=500, docs=60_000, seed=3),
+    "star_plus": lambda: _star_plus(),
+}
+
+
+@pytest.fixture(scope="module", params=list(GRAPHS))
+def pair(request):
+    r = GRAPHS[request.param]()
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    lv = Louvain(r.n, r.src, r.dst, r.w)
+    yield r, og, lv
+    lv.close()
+
+
+def test_csr_build(pair):
+    """Neighbor computation: CSR, loops, δ, W identical to the oracle."""
+    r, og, lv = pair
+    a, b = lv.csr(), og.arrays()
+    assert a["W"] == b["W"]
+    assert np.array_equal(a["row_ptr"], b["row_ptr"])
+    assert np.array_equal(a["loop"], b["loop"])
+    assert np.array_equal(a["delta"], b["delta"])
+    ca, wa = _canon_fast(a["row_ptr"], a["col"], a["w"])
+    assert np.array_equal(ca, b["col"]) and np.array_equal(wa, b["w"])
+
+
+def _states(r, og, rng):
+    n = r.n
+    yield np.arange(n, dtype=np.int32)                            # singletons (sweep 1)
+    lab = np.arange(n, dtype=np.int32)
+    for _ in range(3):                                            # oracle trajectory
+        lab, _ = og.sweep(lab)
+        yield lab.copy()
+    yield rng.integers(0, max(1, n // 7), n).astype(np.int32)     # random coarse state
+    yield rng.integers(0, n, n).astype(np.int32)                  # random fine state
+
+
+def test_sweep_and_merge_parity(pair):
+    """One Jacobi sweep (Alg. 1 body) and one isolated-merge batch from the same snapshot:
+    labels, moved count and the exact Eq. 3 numerators (I2, S2) equal the oracle's."""
+    r, og, lv = pair
+    rng = np.random.default_rng(5)
+    for lab in _states(r, og, rng):
+        m = og.modularity(lab)
+        for mode in (0, 1):
+            got, moved, i2, s2 = lv.sweep(lab, mode)
+            want, wmoved = og.sweep(lab, mode)
+            assert np.array_equal(got, want), (r.name, mode, np.nonzero(got != want)[0][:10])
+            assert moved == wmoved
+            assert (i2, s2) == (m["I2"], m["S2"])
+
+
+def test_contract_parity(pair):
+    """Inducing the new graph: identical CSR, loops, δ' (rows canonicalised)."""
+    r, og, lv = pair
+    lab = np.arange(r.n, dtype=np.int32)
+    for _ in range(2):
+        lab, _ = og.sweep(lab)
+    dense, k = oracle.renumber(lab)
+    a = lv.contract(dense, k)
+    b = og.induce(dense, k).arrays()
+    assert np.array_equal(a["row_ptr"], b["row_ptr"])
+    assert np.array_equal(a["loop"], b["loop"])
+    assert np.array_equal(a["delta"], b["delta"])
+    ca, wa = _canon_fast(a["row_ptr"], a["col"], a["w"])
+    assert np.array_equal(ca, b["col"]) and np.array_equal(wa, b["w"])
+
+
+@pytest.mark.parametrize("stop_rule", [0, 1])
+@pytest.mark.parametrize("merge", [True, False])
+def test_full_run_parity(pair, stop_rule, merge):
+    """Algorithm 2 around Algorithm 1: every level's labels, Q, sweep count and the final
+    partition are identical to the oracle's."""
+    r, og, lv = pair
+    want = oracle.run(og, stop_rule=stop_rule, merge_isolated=merge)
+    with Louvain(r.n, r.src, r.dst, r.w, stop_rule=stop_rule, merge_isolated=merge) as g:
+        g.run()
+        assert g.num_levels == len(want.levels)
+        for l in range(g.num_levels):
+            assert np.array_equal(g.partition(l), want.levels[l]), (r.name, l)
+            assert g.modularity(l) == want.q[l]
+            assert g.level_stats(l)[0] == want.sweeps[l]
+        assert np.array_equal(g.partition(-1), want.final)
+        assert g.modularity(-1) == want.final_q
+
+
+def test_karate_values():
+    """C1: Q in the north_star band; same levels as the oracle with caps 99/100
+    (the Jacobi 2-cycle makes the result depend on the cap's parity, reading D12)."""
+    r = inputs.karate()
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    for cap in (99, 100, 7):
+        want = oracle.run(og, max_sweeps=cap)
+        with Louvain(r.n, r.src, r.dst, max_sweeps=cap) as g:
+            g.run()
+            assert np.array_equal(g.partition(-1), want.final)
+            assert g.modularity() == want.final_q
+    with Louvain(r.n, r.src, r.dst) as g:
+        g.run()
+        assert 0.41 <= g.modularity() <= 0.42
+
+
+def test_theta_schedule_parity():
+    r = inputs.rmat(11, 8, seed=3)
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    sched = [1e-2, 1e-6, 1e-3]
+    want = oracle.run(og, theta_schedule=sched)
+    with Louvain(r.n, r.src, r.dst, r.w, theta_schedule=sched) as g:
+        g.run()
+        assert [g.level_stats(l)[0] for l in range(g.num_levels)] == want.sweeps
+        assert np.array_equal(g.partition(-1), want.final)
+
+
+def test_rmat16_full_run_parity():
+    """Larger power-law case (max degree > 8192 exercises the hub path at every level)."""
+    r = inputs.rmat(16, 16, seed=4)
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    want = oracle.run(og)
+    with Louvain(r.n, r.src, r.dst, r.w) as g:
+        g.run()
+        assert [g.level_stats(l)[0] for l in range(g.num_levels)] == want.sweeps
+        for l in range(g.num_levels):
+            assert np.array_equal(g.partition(l), want.levels[l])
+            assert g.modularity(l) == want.q[l]
+
+
+def test_edge_cases():
+    # loops only / isolated vertices / single edge / duplicates summing
+    for n, s, d, w in [
+        (3, [0, 1], [0, 1], [2, 5]),               # loops only: no moves, one level
+        (5, [0], [1], None),                       # isolated vertices kept (D20)
+        (2, [0, 1, 0], [1, 0, 1], [1, 2, 3]),       # duplicates summed (D25)
+        (1, [0], [0], [4]),                        # single vertex with a loop
+    ]:
+        og = oracle.Graph.from_edges(n, s, d, w)
+        want = oracle.run(og)
+        with Louvain(n, np.array(s), np.array(d), None if w is None else np.array(w, np.int64)) as g:
+            g.run()
+            assert np.array_equal(g.partition(-1), want.final)
+            assert g.modularity() == want.final_q
+            assert g.num_levels == len(want.levels)
+
+
+def test_errors():
+    with pytest.raises(LouvainError) as e:
+        Louvain(3, np.array([0]), np.array([7]))
+    assert e.value.code == 2  # LV_EGRAPH
+    with pytest.raises(LouvainError) as e:
+        Louvain(3, np.array([0]), np.array([1]), np.array([0], np.int64))
+    assert e.value.code == 2
+    with pytest.raises(LouvainError) as e:
+        Louvain(3, np.array([], np.int32), np.array([], np.int32))
+    assert e.value.code == 3  # LV_EZEROW
+    with Louvain(2, np.array([0]), np.array([1])) as g:
+        with pytest.raises(LouvainError) as e:
+            g.partition()
+        assert e.value.code == 7  # LV_ESTATE
+        g.run()
+        with pytest.raises(LouvainError):
+            g.modularity(5)
+
+
+def test_device_inputs_and_repeat_determinism():
+    import torch
+
+    r = inputs.rmat(14, 16, seed=7)
+    with Louvain(r.n, r.src, r.dst, r.w) as a:
+        a.run()
+        pa = a.partition()
+        a.run()
+        assert np.array_equal(a.partition(), pa)
+    s, d, w = (torch.from_numpy(x).cuda() for x in (r.src, r.dst, r.w))
+    with Louvain(r.n, s, d, w) as b:
+        b.run()
+        out = torch.empty(r.n, dtype=torch.int32, device="cuda")
+        b.partition(out=out)
+        assert np.array_equal(out.cpu().numpy(), pa)
