@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the GPU Louvain hot path (arXiv 1805.10904) — one JSON line on rank 0.
+
+A *step* is one pass of the whole hot path over one synthetic graph: louvain_create
+(CSR build from device-resident COO records) + louvain_run (every level: sweeps,
+commit, Q, merge, renumber, contraction) + the final composed partition into a
+device buffer.  value = directed-edge visits of all local-move sweeps of the step /
+step time (edges/s, whole job over all ranks).  e2e = the same through the public API
+from pinned HOST buffers (H2D of the records and D2H of the final partition inside the
+timed region).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                        [--impl {native,reference}]
+Workloads (BASELINE.json configs): karate, sbm, cooc, rmat24 (default), rmat27.
+Inputs are larger than L2 for every workload except karate/sbm (noted in config).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "local-move edges/sec and end-to-end Louvain time at 1/2/4/8 B200; final Q"
+UNIT = "edges/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+# bounded CPU-baseline sample: the oracle's full run (CSR build + all levels) on a
+# smaller graph of the same recipe (10-30 s single-threaded on the GPU box host)
+CPU_SAMPLE = {
+    "rmat24": ("rmat", dict(scale=18, edge_factor=16, seed=4), "R-MAT scale 18, ef 16, weights 1-16 (C4 recipe)"),
+    "rmat27": ("rmat", dict(scale=18, edge_factor=16, seed=5), "R-MAT scale 18, ef 16, weights 1-16 (C5 recipe)"),
+    "sbm": ("sbm", dict(n=100_000, blocks=100, avg_deg=32, mu=0.3, seed=2), "SBM n=100k, blocks of 1000, deg 32, mu 0.3"),
+    "cooc": ("cooc", dict(topics=250, topic_size=1000, docs=875_000, seed=3), "co-occurrence at 1/20 scale (C3 recipe)"),
+    "karate": ("karate", {}, "karate (full workload)"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return dict(PEAKS_FALLBACK)
+
+
+def make_workload(name):
+    from paper_1805_10904_b200 import inputs
+
+    return inputs.make(name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        loaded = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit() and r[6].isdigit() and int(r[6]) > 0]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(loaded or sm) if (loaded or sm) else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=None)
+    return world, rank, local
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def cpu_baseline(workload, budget_note=True):
+    """Time the oracle as it stands (single thread) on a bounded sample of the workload."""
+    import oracle
+    from paper_1805_10904_b200 import inputs
+
+    kind, kw, desc = CPU_SAMPLE[workload]
+    r = getattr(inputs, kind)(**kw)
+    t0 = time.perf_counter()
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    res = oracle.run(g)
+    dt = time.perf_counter() - t0
+    return {"value": res.edge_visits / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle full run (CSR build + all levels) on {desc}: {res.edge_visits} edge visits "
+                      f"in {dt:.2f} s, Q={res.final_q:.6f}", "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, each step a bounded sample."""
+    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass  # the oracle has no warm-up state; one untimed step is not needed
+    times, visits, last = [], 0, None
+    for _ in range(args.steps):
+        b = cpu_baseline(args.workload)
+        times.append(b["seconds"])
+        visits = b["value"] * b["seconds"]
+        last = b
+    T = sum(times) / len(times)
+    line = {"impl": "reference", "metric": METRIC, "value": visits / T, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": T * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample": last["sample"]},
+            "cpu_baseline": {"value": visits / T, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": last["sample"]},
+            "e2e": {"value": visits / T, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="rmat24", choices=["karate", "sbm", "cooc", "rmat24", "rmat27"])
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    from paper_1805_10904_b200 import Louvain
+
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    r = make_workload(args.workload)
+    m = r.m
+    # device-resident inputs (value) and pinned host inputs (e2e)
+    src_d = torch.from_numpy(r.src).to(dev)
+    dst_d = torch.from_numpy(r.dst).to(dev)
+    w_d = None if r.w is None else torch.from_numpy(r.w).to(dev)
+    src_h = torch.from_numpy(r.src).pin_memory()
+    dst_h = torch.from_numpy(r.dst).pin_memory()
+    w_h = None if r.w is None else torch.from_numpy(r.w).pin_memory()
+    out_d = torch.empty(r.n, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False):
+        lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, profile=profile)
+        lv.run()
+        lv.partition(-1, out=out_d)
+        st = lv.run_stats()
+        info = dict(nnz=lv.nnz(), edge_visits=st["edge_visits"], launches=st["launches"], q=lv.modularity(-1),
+                    levels=lv.num_levels, sweeps=[lv.level_stats(l)[0] for l in range(lv.num_levels)],
+                    times=[lv.level_stats(l)[1] for l in range(lv.num_levels)])
+        if profile:
+            info["profile"] = lv.profile()
+        lv.close()
+        return info
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    infos = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        infos.append(step(profile=True))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = allmax(ms, world)
+    visits = infos[-1]["edge_visits"]
+    value = visits * world / (ms / 1e3)
+
+    # e2e through the public API from pinned host buffers (H2D + D2H inside the region)
+    host_out = np.empty(r.n, dtype=np.int32)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        with Louvain(r.n, src_h.numpy(), dst_h.numpy(), None if w_h is None else w_h.numpy(), device=local) as lv:
+            lv.run()
+            host_out[:] = lv.partition(-1)
+    torch.cuda.synchronize()
+    e2e_ms = allmax((time.perf_counter() - t0) * 1e3 / args.e2e_steps, world)
+    h2d = m * (4 + 4 + (0 if r.w is None else r.w.itemsize))
+    d2h = r.n * 4
+
+    # roofline of the dominant kernel over the timed region
+    pk = peaks()
+    agg = {}
+    for inf in infos:
+        for k in inf["profile"]["kernels"]:
+            a = agg.setdefault(k["name"], [0.0, 0.0, 0.0])
+            a[0] += k["ms"]
+            a[1] += k["alg_bytes"]
+            a[2] += k["launches"]
+    top = max(agg, key=lambda k: agg[k][0])
+    t_ms, t_bytes, t_launch = agg[top]
+    achieved = t_bytes / (t_ms / 1e3) / 1e9
+    sweep_ms = sum(v[0] for k, v in agg.items()) / args.steps
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.workload, {}).get(top)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": top,
+                "kernel_ms_per_launch": t_ms / t_launch, "alg_bytes_per_launch": t_bytes / t_launch,
+                "kernel_share_of_step": t_ms / args.steps / ms, "peak_source": pk["source"]}
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline(args.workload)
+            cpu.pop("seconds", None)
+            cpu["cores_note"] = f"single-threaded oracle; host has {os.cpu_count()} cores"
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+    inf = infos[-1]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.workload, "graph": r.name, "n": r.n, "records": m,
+                   "directed_edges": inf["nnz"], "edge_visits_per_step": visits, "levels": inf["levels"],
+                   "sweeps_per_level": inf["sweeps"], "stop_rule": "alg1_abs", "max_sweeps": 100,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (126 MB)" if m * 12 > 126e6 else "inputs fit in L2"},
+        "end_to_end_s": ms / 1e3, "final_q": inf["q"],
+        "sweep_kernels_ms_per_step": sweep_ms,
+        "gpu_launches": inf["launches"],
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": visits * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "clocks": clk,
+        "phase_ms_level0": inf["times"][0],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

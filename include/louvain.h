@@ -91,6 +91,7 @@ typedef struct {
     void *alloc_ctx;
     void *nccl_comm;         /* ncclComm_t for the sweep-sharded path; NULL = 1 GPU     */
     int32_t rank, world;     /* this process's rank / world size in nccl_comm           */
+    int32_t profile;         /* 1: time every sweep kernel with CUDA events during run   */
 } louvain_config;
 
 /* Fill `cfg` with the defaults above. */
@@ -127,8 +128,8 @@ louvain_status louvain_modularity(louvain_t h, int32_t level, double *q);
  * (all sweeps + commits + merge), [3] renumber, [4] induce.  `times` may be NULL. */
 louvain_status louvain_level_stats(louvain_t h, int32_t level, int32_t *sweeps, double *times);
 
-/* Totals of the last run: directed-edge visits of all local-move sweeps, and kernel
- * launches issued by the library. */
+/* directed-edge visits of all local-move sweeps of the last run, and the number of
+ * kernel launches the handle issued since louvain_create (CSR build + every run). */
 louvain_status louvain_run_stats(louvain_t h, int64_t *edge_visits, int64_t *launches);
 
 /* ---- step-level entry points (tests, benchmarks).  Each operates on level 0 of the
@@ -150,6 +151,13 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
  *    "launches"} per kernel, per sweep]}
  * Algorithmic bytes follow DESIGN.md §6.  Errors: LV_EINVAL if cap is too small. */
 louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char *json, int64_t cap);
+
+/* Per-kernel profile of the last run (requires cfg.profile = 1): NUL-terminated JSON
+ *   {"kernels": [{"name", "ms", "alg_bytes", "launches"}], "edge_visits": ...}
+ * with total CUDA-event time and algorithmic bytes per kernel name,
+ * accumulated over every sweep of every level.  Errors: LV_ESTATE (profiling off or no
+ * run), LV_EINVAL (cap too small). */
+louvain_status louvain_profile_json(louvain_t h, char *json, int64_t cap);
 
 /* Level-0 CSR as built on the device (for parity tests): row_ptr (n+1), col (nnz),
  * w (nnz, int64), loop (n), delta (n); host buffers, any may be NULL. */

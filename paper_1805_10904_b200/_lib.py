@@ -20,7 +20,7 @@ LV_W_NONE, LV_W_I32, LV_W_I64 = 0, 1, 2
 EXPORTS = [
     "louvain_config_default", "louvain_create", "louvain_run", "louvain_num_levels", "louvain_level_size",
     "louvain_get_partition", "louvain_modularity", "louvain_level_stats", "louvain_run_stats", "louvain_sweep",
-    "louvain_time_sweeps", "louvain_get_csr", "louvain_contract", "louvain_last_error", "louvain_destroy",
+    "louvain_time_sweeps", "louvain_profile_json", "louvain_get_csr", "louvain_contract", "louvain_last_error", "louvain_destroy",
     "louvain_nccl_unique_id", "louvain_nccl_init", "louvain_nccl_destroy",
 ]
 
@@ -58,6 +58,7 @@ class Config(C.Structure):
         ("nccl_comm", C.c_void_p),
         ("rank", C.c_int32),
         ("world", C.c_int32),
+        ("profile", C.c_int32),
     ]
 
 
@@ -93,6 +94,7 @@ def load() -> C.CDLL:
         "louvain_run_stats": ([P, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "louvain_sweep": ([P, P, P, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(u64)], C.c_int),
         "louvain_time_sweeps": ([P, i32, i32, C.c_char_p, i64], C.c_int),
+        "louvain_profile_json": ([P, C.c_char_p, i64], C.c_int),
         "louvain_get_csr": ([P, C.POINTER(i64), P, P, P, P, P, C.POINTER(i64)], C.c_int),
         "louvain_contract": ([P, P, i64, C.POINTER(i64), P, P, P, P, P], C.c_int),
         "louvain_last_error": ([P], C.c_char_p),

@@ -115,8 +115,41 @@ struct LevelRec {
   double times[5] = {0, 0, 0, 0, 0};
 };
 
+// Per-kernel accumulation of CUDA-event time and algorithmic bytes.
+struct Prof {
+  std::vector<std::string> names;
+  std::vector<double> ms, bytes;
+  std::vector<i64> launches;
+  void add(const std::string &nm, double t, double b) {
+    size_t j = 0;
+    while (j < names.size() && names[j] != nm) ++j;
+    if (j == names.size()) {
+      names.push_back(nm);
+      ms.push_back(0);
+      bytes.push_back(0);
+      launches.push_back(0);
+    }
+    ms[j] += t;
+    bytes[j] += b;
+    launches[j] += 1;
+  }
+  void clear() { names.clear(); ms.clear(); bytes.clear(); launches.clear(); }
+  std::string json(double div) const {
+    std::string js = "[";
+    for (size_t j = 0; j < names.size(); ++j) {
+      char buf[512];
+      snprintf(buf, sizeof(buf), "%s{\"name\": \"%s\", \"ms\": %.6f, \"alg_bytes\": %.1f, \"launches\": %.3f}",
+               j ? ", " : "", names[j].c_str(), ms[j] / div, bytes[j] / div, (double)launches[j] / div);
+      js += buf;
+    }
+    return js + "]";
+  }
+};
+
 struct louvain_ctx {
   Ctx c;
+  Prof prof;
+  bool prof_valid = false;
   bool own_stream = false;
   louvain_config cfg;
   std::vector<double> sched;
@@ -158,6 +191,13 @@ struct SweepOut {
   u128 s2 = 0;
 };
 
+// Algorithmic bytes of one launch of a sweep kernel: per directed edge
+// col 4 + weight wb + neighbour label 4; per distinct candidate deg_C 8; per active
+// vertex 56 (rows[] 4, row_ptr 16, label 4, δ 8, deg_own 8, size_own 4, deg_i 8,
+// label_next 4); commit: 8 B per vertex (two labels) + 56 B per moved vertex.
+double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<struct SweepOut> &pb,
+                        u64 moved);
+
 // Run one pass of MODE over the bins of g (snapshot st.lab[cur] -> st.lab[cur^1]).
 SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int mode, KTimer *tm = nullptr,
                   std::vector<SweepOut> *per_bin = nullptr) {
@@ -196,10 +236,34 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int
   return o;
 }
 
-void commit(louvain_ctx *h, const DGraph &g, State &st) {
+double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<SweepOut> &pb,
+                        u64 moved) {
+  const double wb = wbytes(g.wt);
+  for (int b = 0; b < NSMEM; ++b)
+    if (nm == std::string("sweep:") + BIN_NAME[b])
+      return (double)B.edges[b] * (8.0 + wb) + 8.0 * (double)pb[b].cand + 56.0 * (double)B.count(b);
+  if (nm == "sweep:hub_acc") return (double)B.edges[NSMEM] * (8.0 + wb);
+  if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand + 56.0 * (double)B.count(NSMEM);
+  if (nm == "commit") return 8.0 * (double)g.n + 56.0 * (double)moved;
+  return 0.0;
+}
+
+void account(Prof &P, KTimer &tm, const Bins &B, const DGraph &g, const std::vector<SweepOut> &pb, u64 moved) {
+  for (size_t k = 0; k < tm.names.size(); ++k) {
+    float kt = 0;
+    LV_CUDA(cudaEventSynchronize(tm.ev[2 * k + 1]));
+    LV_CUDA(cudaEventElapsedTime(&kt, tm.ev[2 * k], tm.ev[2 * k + 1]));
+    P.add(tm.names[k], kt, kernel_alg_bytes(tm.names[k], B, g, pb, moved));
+  }
+  tm.clear();
+}
+
+void commit(louvain_ctx *h, const DGraph &g, State &st, KTimer *tm = nullptr) {
   Ctx &c = h->c;
+  if (tm) tm->begin(c.s, "commit");
   LV_LAUNCH(c, k_commit, grid_for(c, g.n), 256, 0, g.n, st.lab[st.cur].p, st.lab[st.cur ^ 1].p, g.delta.p, st.deg.p,
             st.size.p);
+  if (tm) tm->end(c.s);
   st.cur ^= 1;
 }
 
@@ -236,24 +300,34 @@ int32_t one_level(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, dou
   u64 lsum;
   u128 s2i;
   level_consts(h, g, lsum, s2i);
-  SweepOut o = run_pass(h, g, B, st, M_SWEEP);
+  const bool prof = cfg.profile != 0;
+  KTimer tm;
+  tm.on = prof;
+  std::vector<SweepOut> pb;
+  SweepOut o = run_pass(h, g, B, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);
   h->edge_visits += g.nnz;
-  commit(h, g, st);
+  commit(h, g, st, prof ? &tm : nullptr);
+  if (prof) account(h->prof, tm, B, g, pb, o.moved);
   int32_t sweeps = 1;
   if (o.moved == 0) return sweeps;
   bool first = true;
   double Qp = 0.0;
   for (int32_t s = 2; s <= cfg.max_sweeps; ++s) {
-    o = run_pass(h, g, B, st, M_SWEEP);  // tentative sweep s; numerators of state s-1
+    pb.clear();
+    o = run_pass(h, g, B, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);  // tentative sweep s
     h->edge_visits += g.nnz;
-    const i128 I2 = (i128)o.i2 + (i128)2 * (i128)lsum;
+    const i128 I2 = (i128)o.i2 + (i128)2 * (i128)lsum;  // numerators of state s-1
     const i128 S2 = (i128)(o.s2 + s2i);
     const double Q = q_from(g.W, I2, S2);
     const bool stop = !first && stop_test(cfg.stop_rule, Q, Qp, theta);
     first = false;
     Qp = Q;
-    if (stop) break;  // drop sweep s: the literal algorithm stopped after s-1
-    commit(h, g, st);
+    if (stop) {  // drop sweep s: the literal algorithm stopped after s-1
+      if (prof) account(h->prof, tm, B, g, pb, 0);
+      break;
+    }
+    commit(h, g, st, prof ? &tm : nullptr);
+    if (prof) account(h->prof, tm, B, g, pb, o.moved);
     sweeps = s;
     if (o.moved == 0) break;
   }
@@ -280,6 +354,8 @@ void run_impl(louvain_ctx *h) {
   h->final_part.release();
   h->ran = false;
   h->edge_visits = 0;
+  h->prof.clear();
+  h->prof_valid = h->cfg.profile != 0;
   const i64 l0 = c.launches;
   std::unique_ptr<DGraph> owned;
   const DGraph *g = &h->g0;
@@ -503,7 +579,7 @@ louvain_status louvain_level_stats(louvain_t h, int32_t level, int32_t *sweeps, 
 louvain_status louvain_run_stats(louvain_t h, int64_t *edge_visits, int64_t *launches) {
   if (!h) return LV_EINVAL;
   if (edge_visits) *edge_visits = h->edge_visits;
-  if (launches) *launches = h->run_launches;
+  if (launches) *launches = h->c.launches;  // all launches since create (CSR build + run)
   return LV_OK;
 }
 
@@ -533,7 +609,13 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
     LV_REQUIRE(herr == 0, LV_EINVAL, "labels must lie in [0,n)");
-    SweepOut o = run_pass(h, g, B, st, mode == 0 ? M_SWEEP : M_MERGE);
+    // the sweep pass also yields Σ e_{i->C(i)} of the snapshot; merge mode reuses it
+    SweepOut o = run_pass(h, g, B, st, M_SWEEP);
+    if (mode == 1) {
+      const u64 i2_snap = o.i2;
+      o = run_pass(h, g, B, st, M_MERGE);
+      o.i2 = i2_snap;
+    }
     // exact Eq. 3 numerators of the snapshot (S2 over all labels, not the fused form)
     u64 lsum;
     u128 s2i;
@@ -573,78 +655,45 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
     LV_CUDA(cudaStreamSynchronize(c.s));
     KTimer tm;
     tm.on = true;
+    Prof P;
     cudaEvent_t e0, e1;
     LV_CUDA(cudaEventCreate(&e0));
     LV_CUDA(cudaEventCreate(&e1));
     double total_ms = 0;
-    std::vector<std::string> knames;
-    std::vector<double> kms, kbytes;
-    std::vector<i64> klaunch;
-    double alg_total = 0;
-    const int wb = wbytes(g.wt);
     for (int r = 0; r < reps; ++r) {
-      tm.clear();
       std::vector<SweepOut> pb;
       LV_CUDA(cudaEventRecord(e0, c.s));
       SweepOut o = run_pass(h, g, B, st, M_SWEEP, &tm, &pb);  // includes the counter D2H sync
-      tm.begin(c.s, "commit");
-      commit(h, g, st);
-      tm.end(c.s);
+      commit(h, g, st, &tm);
       LV_CUDA(cudaEventRecord(e1, c.s));
       LV_CUDA(cudaEventSynchronize(e1));
       float ms = 0;
       LV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       total_ms += ms;
-      // per-kernel times and algorithmic bytes
-      for (size_t k = 0; k < tm.names.size(); ++k) {
-        float kt = 0;
-        LV_CUDA(cudaEventElapsedTime(&kt, tm.ev[2 * k], tm.ev[2 * k + 1]));
-        const std::string &nm = tm.names[k];
-        double bytes = 0;
-        int bin = -1;
-        for (int b = 0; b < NSMEM; ++b)
-          if (nm == std::string("sweep:") + BIN_NAME[b]) bin = b;
-        if (bin >= 0) {
-          bytes = (double)B.edges[bin] * (8.0 + wb) + 8.0 * (double)pb[bin].cand + 48.0 * (double)B.count(bin);
-        } else if (nm == "sweep:hub_acc") {
-          bytes = (double)B.edges[NSMEM] * (8.0 + wb);
-        } else if (nm == "sweep:hub_fin") {
-          bytes = 8.0 * (double)pb[NSMEM].cand + 48.0 * (double)B.count(NSMEM);
-        } else if (nm == "commit") {
-          bytes = 8.0 * (double)g.n + 24.0 * (double)o.moved;
-        }
-        size_t j = 0;
-        while (j < knames.size() && knames[j] != nm) ++j;
-        if (j == knames.size()) {
-          knames.push_back(nm);
-          kms.push_back(0);
-          kbytes.push_back(0);
-          klaunch.push_back(0);
-        }
-        kms[j] += kt;
-        kbytes[j] += bytes;
-        klaunch[j] += 1;
-        alg_total += bytes;
-      }
+      account(P, tm, B, g, pb, o.moved);
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    double alg = 0;
+    for (double b : P.bytes) alg += b;
     std::string js = "{\"ms_sweep\": " + std::to_string(total_ms / reps) +
-                     ", \"alg_bytes_sweep\": " + std::to_string(alg_total / reps) +
+                     ", \"alg_bytes_sweep\": " + std::to_string(alg / reps) +
                      ", \"edges\": " + std::to_string(g.nnz) + ", \"n\": " + std::to_string(g.n) +
-                     ", \"active\": " + std::to_string(B.active()) + ", \"kernels\": [";
-    for (size_t j = 0; j < knames.size(); ++j) {
-      char buf[512];
-      snprintf(buf, sizeof(buf), "%s{\"name\": \"%s\", \"ms\": %.6f, \"alg_bytes\": %.1f, \"launches\": %lld}",
-               j ? ", " : "", knames[j].c_str(), kms[j] / reps, kbytes[j] / reps, (long long)(klaunch[j] / reps));
-      js += buf;
-    }
-    js += "]}";
+                     ", \"active\": " + std::to_string(B.active()) + ", \"kernels\": " + P.json(reps) + "}";
     if ((int64_t)js.size() + 1 > cap) return LV_EINVAL;
     memcpy(json, js.c_str(), js.size() + 1);
   } catch (const Error &e) {
     return fail(h, e);
   }
+  return LV_OK;
+}
+
+louvain_status louvain_profile_json(louvain_t h, char *json, int64_t cap) {
+  if (!h || !json) return LV_EINVAL;
+  if (!h->ran || !h->prof_valid) return LV_ESTATE;
+  std::string js = "{\"edge_visits\": " + std::to_string(h->edge_visits) + ", \"kernels\": " + h->prof.json(1.0) + "}";
+  if ((int64_t)js.size() + 1 > cap) return LV_EINVAL;
+  memcpy(json, js.c_str(), js.size() + 1);
   return LV_OK;
 }
 

@@ -201,7 +201,7 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
   const size_t smem = (size_t)GPB * CAP * (sizeof(u64) + sizeof(int32_t));
   static int occ = -1;
   if (occ < 0) {
-    if (smem > 48 * 1024) LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int o = 0;
     LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, smem));
     occ = o > 0 ? o : 1;

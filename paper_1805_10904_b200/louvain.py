@@ -80,14 +80,14 @@ class Louvain:
 
     def __init__(self, n, src, dst, w=None, *, device=0, stream=None, torch_allocator=True,
                  theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64, stop_rule=0,
-                 merge_isolated=True, theta_schedule=None, nccl_comm=None, rank=0, world=1):
+                 merge_isolated=True, theta_schedule=None, nccl_comm=None, rank=0, world=1, profile=False):
         self._lib = _lib.load()
         self._h = C.c_void_p()
         self._keep = []
         cfg = default_config(theta=float(theta), big_theta=float(big_theta), max_sweeps=int(max_sweeps),
                              max_levels=int(max_levels), stop_rule=int(stop_rule),
                              merge_isolated=int(bool(merge_isolated)), device=int(device), rank=int(rank),
-                             world=int(world))
+                             world=int(world), profile=int(bool(profile)))
         if theta_schedule:
             arr = (C.c_double * len(theta_schedule))(*[float(x) for x in theta_schedule])
             self._keep.append(arr)
@@ -218,6 +218,17 @@ class Louvain:
         buf = C.create_string_buffer(_CAP)
         check(self._lib.louvain_time_sweeps(self._h, int(warm), int(reps), buf, _CAP), self._h)
         return json.loads(buf.value.decode())
+
+    def profile(self) -> dict:
+        buf = C.create_string_buffer(_CAP)
+        check(self._lib.louvain_profile_json(self._h, buf, _CAP), self._h)
+        return json.loads(buf.value.decode())
+
+    def nnz(self) -> int:
+        """Directed non-loop adjacency entries of the level-0 CSR."""
+        nnz, W = C.c_int64(), C.c_int64()
+        check(self._lib.louvain_get_csr(self._h, C.byref(nnz), None, None, None, None, None, C.byref(W)), self._h)
+        return nnz.value
 
     def csr(self) -> dict:
         nnz, W = C.c_int64(), C.c_int64()
