@@ -83,19 +83,45 @@ __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
   return ((uint32_t)k * 0x9E3779B1u) >> (32 - lg);
 }
 
-// Open-addressing insert with linear probing; keys -1 = empty.  Exact u64 add.
-__device__ __forceinline__ void tab_insert(int32_t *keys, u64 *vals, unsigned mask, int lg, int32_t k, u64 v) {
+// Exact 64-bit add (mod 2^64) with native 32-bit atomics: sm_100 has no native 64-bit
+// shared-memory add (it compiles to a CAS loop, which collapses under the same-key
+// contention of later sweeps); the low word's returned old value gives the carry.
+__device__ __forceinline__ void add_u64_split(u64 *p, u64 v) {
+  uint32_t *q = (uint32_t *)p;
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(q, lo);
+  const uint32_t carry = ((uint32_t)(old + lo) < old) ? 1u : 0u;
+  if (hi + carry) atomicAdd(q + 1, hi + carry);
+}
+
+// Open-addressing insert with linear probing; keys -1 = empty.  Returns the slot.
+template <bool SHARED>
+__device__ __forceinline__ unsigned tab_insert(int32_t *keys, u64 *vals, unsigned mask, int lg, int32_t k, u64 v,
+                                               bool *claimed = nullptr) {
   unsigned h = hslot(k, lg);
   while (true) {
     int32_t cur = ((volatile int32_t *)keys)[h];
     if (cur == k) break;
     if (cur == -1) {
       int32_t old = atomicCAS(&keys[h], -1, k);
-      if (old == -1 || old == k) break;
+      if (old == -1) {
+        if (claimed) *claimed = true;
+        break;
+      }
+      if (old == k) break;
     }
     h = (h + 1) & mask;
   }
-  atomicAdd(&vals[h], v);
+  if (SHARED) add_u64_split(&vals[h], v);
+  else atomicAdd(&vals[h], v);
+  return h;
+}
+
+// smallest lg with 2^lg >= 2*d (d >= 1), clamped to [3, LGMAX]
+__device__ __forceinline__ int row_lg(i64 d, int lgmax) {
+  int lg = 64 - __clzll((unsigned long long)(2 * d - 1));
+  lg = lg < 3 ? 3 : lg;
+  return lg > lgmax ? lgmax : lg;
 }
 
 // ----------------------------------------------------------------- group primitives
@@ -360,52 +386,215 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
         continue;
       }
     }
+    const int lg = row_lg(end - beg, LG);  // table prefix sized for this row
+    const unsigned mask = (1u << lg) - 1u;
     for (i64 e = beg + g.lane; e < end; e += G) {
       int32_t k = __ldg(&a.keys[e]);
       if (MODE != M_EMIT) k = __ldg(&a.label[k]);
-      tab_insert(keys, vals, CAP - 1, LG, k, WT::get(a.w, e));
+      tab_insert<true>(keys, vals, mask, lg, k, WT::get(a.w, e));
     }
     g.sync();
-    row_epilogue<G, BLOCK, MODE>(g, keys, vals, CAP, r, own, a, acc);
+    row_epilogue<G, BLOCK, MODE>(g, keys, vals, (i64)1 << lg, r, own, a, acc);
     g.sync();
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
 
 // ----------------------------------------------------------------- hub path
-constexpr int HUB_ACC_T = 256;
-constexpr int HUB_FIN_T = 512;
+// Rows longer than the largest shared-memory bin.  Per hub row h:
+//   k_hub_acc    one CTA per HUB_CHUNK edges: aggregate the chunk in a shared-memory table,
+//                then flush its distinct (key, Σw) into the row's global table; a slot
+//                claimed for the first time is appended to the row's occupied list.
+//   k_hub_fin    nparts CTAs per row, each over a strided share of the occupied list:
+//                score / count / emit, reset the slots, write one partial per CTA.
+//   k_hub_decide one thread per row: combine the partials, decide, reset the row's counters.
+constexpr int HUB_ACC_T = 512;
+constexpr int HUB_SM_LG = 13;  // 8192-slot pre-aggregation table (chunk of 4096 edges)
+constexpr int HUB_FIN_T = 256;
+constexpr i64 HUB_FIN_PER = 8192;  // occupied entries per fin CTA
+
+struct FinChunk {
+  int32_t h, j, nparts, pad;
+};
+
+struct HubPartial {
+  i64 hi;
+  u64 lo;
+  int32_t c, T;
+  u64 eown, cnt, selfw, sumw;
+};
+
+struct HubArgs {
+  const FinChunk *fchunks;
+  const i64 *pstart;    // first partial of hub h
+  const int32_t *nparts;
+  int32_t *occ;         // occupied-slot lists (offset toff[h]/2)
+  uint32_t *occ_cnt;    // per hub
+  u64 *emit_cur;        // per hub (EMIT output cursor)
+  HubPartial *part;
+  i64 nhub;
+};
 
 template <int MODE, class WT>
-__global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a) {
+__global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  constexpr int CAPS = 1 << HUB_SM_LG;
+  u64 *svals = (u64 *)sm;
+  int32_t *skeys = (int32_t *)(sm + (size_t)CAPS * sizeof(u64));
   const Chunk ch = a.chunks[blockIdx.x];
   const int32_t r = a.rows[ch.h];
   if (MODE == M_MERGE) {
     if (a.size[a.label[r]] != 1) return;
   }
-  const int lg = a.tlog[ch.h];
-  int32_t *keys = a.tkeys + a.toff[ch.h];
-  u64 *vals = a.tvals + a.toff[ch.h];
-  const unsigned mask = (1u << lg) - 1u;
+  for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
+  __syncthreads();
   for (i64 e = ch.beg + threadIdx.x; e < ch.end; e += HUB_ACC_T) {
     int32_t k = __ldg(&a.keys[e]);
     if (MODE != M_EMIT) k = __ldg(&a.label[k]);
-    tab_insert(keys, vals, mask, lg, k, WT::get(a.w, e));
+    tab_insert<true>(skeys, svals, CAPS - 1, HUB_SM_LG, k, WT::get(a.w, e));
+  }
+  __syncthreads();
+  const int lg = a.tlog[ch.h];
+  const i64 off = a.toff[ch.h];
+  int32_t *gk = a.tkeys + off;
+  u64 *gv = a.tvals + off;
+  int32_t *occ = hb.occ + off / 2;
+  const unsigned mask = (1u << lg) - 1u;
+  for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) {
+    const int32_t k = skeys[s];
+    if (k >= 0) {
+      bool claimed = false;
+      const unsigned slot = tab_insert<false>(gk, gv, mask, lg, k, svals[s], &claimed);
+      if (claimed) occ[atomicAdd(&hb.occ_cnt[ch.h], 1u)] = (int32_t)slot;
+    }
   }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a) {
-  const int h = blockIdx.x;
+__global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
+  const FinChunk fc = hb.fchunks[blockIdx.x];
+  const int h = fc.h;
   const int32_t r = a.rows[h];
   const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
-  Acc acc;
-  if (MODE == M_MERGE && a.size[own] != 1) {
-    if (threadIdx.x == 0) a.label_next[r] = own;
-  } else {
+  HubPartial P;
+  P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1;
+  P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
+  const bool skip = (MODE == M_MERGE) && a.size[own] != 1;
+  if (!skip) {
+    const i64 off = a.toff[h];
+    int32_t *gk = a.tkeys + off;
+    u64 *gv = a.tvals + off;
+    const int32_t *occ = hb.occ + off / 2;
+    const int32_t cnt = (int32_t)hb.occ_cnt[h];
+    const int stride = fc.nparts * HUB_FIN_T;
+    Cand best;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    u64 eown = 0, n1 = 0, selfw = 0, sumw = 0;
+    int32_t T = -1;
+    const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
+    for (int t = fc.j * HUB_FIN_T + threadIdx.x; t < cnt; t += stride) {
+      const int32_t slot = occ[t];
+      const int32_t k = gk[slot];
+      const u64 v = gv[slot];
+      if (MODE != M_EMIT) { gk[slot] = -1; gv[slot] = 0; }
+      if (MODE == M_SWEEP) {
+        if (k == own) eown = v;
+        else {
+          ++n1;
+          i128 S = (i128)a.twoW * (i128)(i64)v - (i128)di * (i128)__ldg(&a.deg[k]);
+          Cand x;
+          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k;
+          if (cand_better(x, best)) best = x;
+        }
+      } else if (MODE == M_MERGE) {
+        if (k != own) { ++n1; T = max(T, k); }
+      } else {
+        sumw += v;
+        if (k == r) selfw += v;
+        else ++n1;
+      }
+    }
+    if (MODE == M_EMIT) {
+      // second pass: write this CTA's entries at a cursor reserved for the CTA
+      u64 tot;
+      Grp<HUB_FIN_T, HUB_FIN_T> g;
+      const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
+      __shared__ u64 sbase;
+      if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
+      __syncthreads();
+      i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
+      for (int t = fc.j * HUB_FIN_T + threadIdx.x; t < cnt; t += stride) {
+        const int32_t slot = occ[t];
+        const int32_t k = gk[slot];
+        const u64 v = gv[slot];
+        gk[slot] = -1;
+        gv[slot] = 0;
+        if (k != r && a.out_key) {
+          a.out_key[o] = k;
+          a.out_w[o] = v;
+          ++o;
+        }
+      }
+    }
     Grp<HUB_FIN_T, HUB_FIN_T> g;
-    row_epilogue<HUB_FIN_T, HUB_FIN_T, MODE>(g, a.tkeys + a.toff[h], a.tvals + a.toff[h],
-                                             (i64)1 << a.tlog[h], r, own, a, acc);
+    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, T);
+    Cand none;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    int32_t dummy = 0;
+    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dummy);
+    if (threadIdx.x == 0) {
+      P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.T = T;
+      P.eown = eown; P.cnt = n1; P.selfw = selfw; P.sumw = sumw;
+    }
+  }
+  if (threadIdx.x == 0) hb.part[hb.pstart[h] + fc.j] = P;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
+  Acc acc;
+  const i64 h = (i64)blockIdx.x * 128 + threadIdx.x;
+  if (h < hb.nhub) {
+    const int32_t r = a.rows[h];
+    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    Cand best;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    u64 eown = 0, cnt = 0, selfw = 0, sumw = 0;
+    int32_t T = -1;
+    const HubPartial *p = hb.part + hb.pstart[h];
+    for (int j = 0; j < hb.nparts[h]; ++j) {
+      Cand x;
+      x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
+      if (cand_better(x, best)) best = x;
+      eown += p[j].eown; cnt += p[j].cnt; selfw += p[j].selfw; sumw += p[j].sumw;
+      T = max(T, p[j].T);
+    }
+    if (MODE == M_SWEEP) {
+      const i64 di = a.delta[r];
+      const i64 dq = a.deg[own];
+      i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
+      int32_t tgt = own;
+      if (best.c != INT32_MAX && cand_S(best) > S_own) {
+        tgt = best.c;
+        if (a.size[own] == 1 && a.size[best.c] == 1 && best.c > own) tgt = own;
+      }
+      a.label_next[r] = tgt;
+      acc.moved += (tgt != own);
+      acc.i2 += eown;
+      acc.cand += cnt;
+      acc.add_sq(a.deg[r]);
+    } else if (MODE == M_MERGE) {
+      int32_t tgt = own;
+      if (a.size[own] == 1 && cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
+      a.label_next[r] = tgt;
+      acc.moved += (tgt != own);
+    } else {
+      a.out_cnt[r] = (i64)cnt;
+      if (a.out_self) a.out_self[r] = selfw;
+      if (a.out_sum) a.out_sum[r] = sumw;
+    }
+    hb.occ_cnt[h] = 0;
+    hb.emit_cur[h] = 0;
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }

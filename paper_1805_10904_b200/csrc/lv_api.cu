@@ -243,7 +243,8 @@ double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, c
     if (nm == std::string("sweep:") + BIN_NAME[b])
       return (double)B.edges[b] * (8.0 + wb) + 8.0 * (double)pb[b].cand + 56.0 * (double)B.count(b);
   if (nm == "sweep:hub_acc") return (double)B.edges[NSMEM] * (8.0 + wb);
-  if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand + 56.0 * (double)B.count(NSMEM);
+  if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand;
+  if (nm == "sweep:hub_decide") return 56.0 * (double)B.count(NSMEM);
   if (nm == "commit") return 8.0 * (double)g.n + 56.0 * (double)moved;
   return 0.0;
 }

@@ -69,6 +69,14 @@ struct Bins {
   Buf<Chunk> chunks;
   Buf<int32_t> tkeys;
   Buf<u64> tvals;
+  i64 nfin = 0;
+  Buf<FinChunk> fchunks;
+  Buf<i64> pstart;
+  Buf<int32_t> nparts;
+  Buf<int32_t> occ;
+  Buf<uint32_t> occ_cnt;
+  Buf<u64> emit_cur;
+  Buf<HubPartial> part;
   i64 count(int b) const { return off[b + 1] - off[b]; }
   i64 active() const { return off[NBIN]; }
 };
@@ -159,11 +167,13 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
     LV_CUDA(cudaMemcpyAsync(beg.data(), hb.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaMemcpyAsync(len.data(), hl.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
-    std::vector<i64> toff(B.nhub);
-    std::vector<int32_t> tlog(B.nhub);
+    std::vector<i64> toff(B.nhub), pstart(B.nhub);
+    std::vector<int32_t> tlog(B.nhub), nparts(B.nhub);
     std::vector<Chunk> ch;
+    std::vector<FinChunk> fch;
     for (i64 h = 0; h < B.nhub; ++h) {
-      i64 want = 2 * std::min(len[h], universe);
+      const i64 distinct_max = std::min(len[h], universe);
+      i64 want = 2 * distinct_max;
       int lg = 5;
       while (((i64)1 << lg) < want) ++lg;
       tlog[h] = lg;
@@ -177,18 +187,34 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
         k.pad = 0;
         ch.push_back(k);
       }
+      nparts[h] = (int32_t)std::max<i64>(1, cdiv(distinct_max, HUB_FIN_PER));
+      pstart[h] = (i64)fch.size();
+      for (int32_t j = 0; j < nparts[h]; ++j) fch.push_back(FinChunk{(int32_t)h, j, nparts[h], 0});
     }
     B.nchunks = (i64)ch.size();
+    B.nfin = (i64)fch.size();
     B.toff.alloc(c.A, B.nhub);
     B.tlog.alloc(c.A, B.nhub);
     B.chunks.alloc(c.A, B.nchunks);
     B.tkeys.alloc(c.A, B.tslots);
     B.tvals.alloc(c.A, B.tslots);
+    B.fchunks.alloc(c.A, B.nfin);
+    B.pstart.alloc(c.A, B.nhub);
+    B.nparts.alloc(c.A, B.nhub);
+    B.occ.alloc(c.A, B.tslots / 2);
+    B.occ_cnt.alloc(c.A, B.nhub);
+    B.emit_cur.alloc(c.A, B.nhub);
+    B.part.alloc(c.A, B.nfin);
     LV_CUDA(cudaMemcpyAsync(B.toff.p, toff.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.tlog.p, tlog.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.chunks.p, ch.data(), B.nchunks * sizeof(Chunk), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.fchunks.p, fch.data(), B.nfin * sizeof(FinChunk), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.pstart.p, pstart.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.nparts.p, nparts.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemsetAsync(B.tkeys.p, 0xff, B.tslots * sizeof(int32_t), c.s));
     LV_CUDA(cudaMemsetAsync(B.tvals.p, 0, B.tslots * sizeof(u64), c.s));
+    LV_CUDA(cudaMemsetAsync(B.occ_cnt.p, 0, B.nhub * sizeof(uint32_t), c.s));
+    LV_CUDA(cudaMemsetAsync(B.emit_cur.p, 0, B.nhub * sizeof(u64), c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));  // host vectors go out of scope
   }
 }
@@ -237,11 +263,29 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     a.toff = B.toff.p;
     a.tlog = B.tlog.p;
     a.chunks = B.chunks.p;
+    HubArgs hb;
+    hb.fchunks = B.fchunks.p;
+    hb.pstart = B.pstart.p;
+    hb.nparts = B.nparts.p;
+    hb.occ = B.occ.p;
+    hb.occ_cnt = B.occ_cnt.p;
+    hb.emit_cur = B.emit_cur.p;
+    hb.part = B.part.p;
+    hb.nhub = B.nhub;
+    const size_t smem = (size_t)(1 << HUB_SM_LG) * (sizeof(u64) + sizeof(int32_t));
+    static bool attr = false;
+    if (!attr) {
+      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
     if (tm) tm->begin(c.s, pre + "hub_acc");
-    LV_LAUNCH(c, (k_hub_acc<MODE, WT>), (unsigned)B.nchunks, HUB_ACC_T, 0, a);
+    LV_LAUNCH(c, (k_hub_acc<MODE, WT>), (unsigned)B.nchunks, HUB_ACC_T, smem, a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_fin");
-    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nhub, HUB_FIN_T, 0, a);
+    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nfin, HUB_FIN_T, 0, a, hb);
+    if (tm) tm->end(c.s);
+    if (tm) tm->begin(c.s, pre + "hub_decide");
+    LV_LAUNCH(c, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
     if (tm) tm->end(c.s);
   }
   if (B.count(7)) { set(7); launch_bin<512, 16384, 512, MODE, WT>(c, tm, a, (pre + BIN_NAME[7]).c_str()); }
