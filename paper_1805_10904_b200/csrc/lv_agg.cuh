@@ -124,6 +124,40 @@ __device__ __forceinline__ int row_lg(i64 d, int lgmax) {
   return lg > lgmax ? lgmax : lg;
 }
 
+// Insert the row's edges [beg, end) into a table, U edges per lane per batch so the
+// col/w loads and then the label gathers of a batch are independent and in flight
+// together (memory-level parallelism; the atomics would otherwise serialise them).
+template <int G, int U, int MODE, class WT, bool SHARED, bool LIST>
+__device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, u64 *vals,
+                                             unsigned mask, int lg, uint16_t *olist, int *ocnt) {
+  for (i64 e0 = beg + lane; e0 < end; e0 += (i64)G * U) {
+    int32_t k[U];
+    u64 wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 e = e0 + (i64)u * G;
+      k[u] = -1;
+      wv[u] = 0;
+      if (e < end) {
+        k[u] = __ldg(&a.keys[e]);
+        wv[u] = WT::get(a.w, e);
+      }
+    }
+    if (MODE != 2 /* M_EMIT */) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k[u] >= 0) k[u] = __ldg(&a.label[k[u]]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k[u] < 0) continue;
+      bool claimed = false;
+      const unsigned sl = tab_insert<SHARED>(keys, vals, mask, lg, k[u], wv[u], LIST ? &claimed : nullptr);
+      if (LIST && claimed) olist[atomicAdd(ocnt, 1)] = (uint16_t)sl;
+    }
+  }
+}
+
 // ----------------------------------------------------------------- group primitives
 // A "group" is the set of G threads that cooperate on one row: a segment of a warp
 // (G <= 32) or the whole CTA (G == BLOCK > 32).
@@ -255,59 +289,85 @@ struct Acc {
 };
 
 // ----------------------------------------------------------------- row epilogue
-// Scans the row's table (capacity cap), resets every slot it reads, and applies the
-// mode's epilogue.  Slots are visited by lane-strided order, identically in both passes.
-template <int G, int BLOCK, int MODE>
-__device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, u64 *vals, i64 cap,
-                                             int32_t r, int32_t own, const AggArgs &a, Acc &acc) {
+// Per-row scalars the group's lane 0 prefetches before the insertion loop (SWEEP).
+struct RowPre {
+  i64 dq = 0, dr = 0;  // deg_own, deg_r
+  int32_t szo = 0;     // |own|
+};
+
+// Visits the row's occupied entries — by scanning slots [0,n) (LIST = false) or through
+// the occupied-slot list olist[0..n) (LIST = true) — resets every slot it reads, and
+// applies the mode's epilogue.  Both EMIT passes visit entries in the same order.
+template <int G, int BLOCK, int MODE, bool LIST, class SlotT>
+__device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, u64 *vals, const SlotT *olist,
+                                             i64 n, int32_t r, int32_t own, i64 di, const RowPre &pre,
+                                             const AggArgs &a, Acc &acc) {
+  constexpr int U = G < 32 ? 2 : 4;  // entries per lane per batch: their deg_C gathers overlap
   if (MODE == M_SWEEP) {
-    const i64 di = a.delta[r];
     Cand best;
     best.hi = 0; best.lo = 0; best.c = INT32_MAX;
     u64 eown = 0, ncand = 0;
     int32_t dummy = 0;
-    for (i64 s = g.lane; s < cap; s += G) {
-      int32_t k = keys[s];
-      if (k >= 0) {
-        u64 v = vals[s];
-        keys[s] = -1;
-        vals[s] = 0;
-        if (k == own) {
-          eown = v;
+    for (i64 t0 = g.lane; t0 < n; t0 += (i64)G * U) {
+      int32_t sl[U], k[U];
+      u64 v[U];
+      i64 dk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const i64 t = t0 + (i64)u * G;
+        sl[u] = t < n ? (LIST ? (int32_t)olist[t] : (int32_t)t) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        k[u] = sl[u] >= 0 ? keys[sl[u]] : -1;
+        v[u] = 0;
+        if (k[u] >= 0) {
+          v[u] = vals[sl[u]];
+          keys[sl[u]] = -1;
+          vals[sl[u]] = 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k[u] < 0) continue;
+        if (k[u] == own) {
+          eown = v[u];
         } else {
           ++ncand;
-          i128 S = (i128)a.twoW * (i128)(i64)v - (i128)di * (i128)__ldg(&a.deg[k]);
+          i128 S = (i128)a.twoW * (i128)(i64)v[u] - (i128)di * (i128)dk[u];
           Cand x;
-          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k;
+          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
           if (cand_better(x, best)) best = x;
         }
       }
     }
     grp_reduce<G, BLOCK>(g, best, eown, ncand, dummy);
     if (g.lane == 0) {
-      const i64 dq = a.deg[own];
-      i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
+      i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)pre.dq - (i128)di);
       int32_t tgt = own;
       if (best.c != INT32_MAX && cand_S(best) > S_own) {
         tgt = best.c;
-        if (a.size[own] == 1 && a.size[best.c] == 1 && best.c > own) tgt = own;  // singlet rule
+        if (pre.szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule
       }
       a.label_next[r] = tgt;
       acc.moved += (tgt != own);
       acc.i2 += eown;
       acc.cand += ncand;
-      acc.add_sq(a.deg[r]);  // deg of label index r: Σ over all labels gives S2
+      acc.add_sq(pre.dr);  // deg of label index r: Σ over all labels gives S2
     }
   } else if (MODE == M_MERGE) {
     Cand none;
     none.hi = 0; none.lo = 0; none.c = INT32_MAX;
     u64 cnt = 0, unused = 0;
     int32_t T = -1;
-    for (i64 s = g.lane; s < cap; s += G) {
-      int32_t k = keys[s];
+    for (i64 t = g.lane; t < n; t += G) {
+      const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
+      const int32_t k = keys[sl];
       if (k >= 0) {
-        keys[s] = -1;
-        vals[s] = 0;
+        keys[sl] = -1;
+        vals[sl] = 0;
         if (k != own) { ++cnt; T = max(T, k); }
       }
     }
@@ -320,24 +380,26 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
     }
   } else {  // M_EMIT
     u64 c = 0, selfw = 0, sumw = 0;
-    for (i64 s = g.lane; s < cap; s += G) {
-      int32_t k = keys[s];
+    for (i64 t = g.lane; t < n; t += G) {
+      const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
+      const int32_t k = keys[sl];
       if (k >= 0) {
-        u64 v = vals[s];
+        const u64 v = vals[sl];
         sumw += v;
         if (k == r) selfw += v;
         else ++c;
       }
     }
     u64 tot;
-    u64 pre = grp_excl_scan<G, BLOCK>(g, c, tot);
-    i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)pre;
-    for (i64 s = g.lane; s < cap; s += G) {
-      int32_t k = keys[s];
+    const u64 pre_ = grp_excl_scan<G, BLOCK>(g, c, tot);
+    i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)pre_;
+    for (i64 t = g.lane; t < n; t += G) {
+      const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
+      const int32_t k = keys[sl];
       if (k >= 0) {
-        u64 v = vals[s];
-        keys[s] = -1;
-        vals[s] = 0;
+        const u64 v = vals[sl];
+        keys[sl] = -1;
+        vals[sl] = 0;
         if (k != r && a.out_key) {
           a.out_key[o] = k;
           a.out_w[o] = v;
@@ -358,9 +420,19 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
 }
 
 // ----------------------------------------------------------------- shared-memory bins
+// Tables of CAP >= 256 slots keep an occupied-slot list (uint16 indices) so the
+// epilogue costs O(distinct keys), not O(capacity).
+template <int CAP>
+constexpr bool has_list() { return CAP >= 256; }
+template <int G, int CAP, int BLOCK>
+constexpr size_t smem_bytes() {
+  return (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(u64) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) + 16);
+}
+
 template <int G, int CAP, int BLOCK, int MODE, class WT>
 __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   constexpr int GPB = BLOCK / G;
+  constexpr bool LIST = has_list<CAP>();
   constexpr int LG = (CAP >= 65536) ? 16 : (CAP >= 32768) ? 15 : (CAP >= 16384) ? 14 : (CAP >= 8192) ? 13
                    : (CAP >= 4096) ? 12 : (CAP >= 2048) ? 11 : (CAP >= 1024) ? 10 : (CAP >= 512) ? 9
                    : (CAP >= 256) ? 8 : (CAP >= 128) ? 7 : (CAP >= 64) ? 6 : (CAP >= 32) ? 5
@@ -369,17 +441,29 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   u64 *svals = (u64 *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)GPB * CAP * sizeof(u64));
+  uint16_t *slist = (uint16_t *)(sm + (size_t)GPB * CAP * 12);
+  int *scnt = (int *)(sm + (size_t)GPB * CAP * 12 + (LIST ? (size_t)GPB * CAP : 0));
   Grp<G, BLOCK> g;
   const int grp = threadIdx.x / G;
   int32_t *keys = skeys + grp * CAP;
   u64 *vals = svals + grp * CAP;
+  uint16_t *olist = slist + grp * (CAP / 2);
+  int *ocnt = scnt + grp;
   Acc acc;
   for (int s = g.lane; s < CAP; s += G) { keys[s] = -1; vals[s] = 0; }
+  if (LIST && g.lane == 0) *ocnt = 0;
   g.sync();
   for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < a.nrows; idx += (i64)gridDim.x * GPB) {
     const int32_t r = a.rows[idx];
     const i64 beg = a.ptr[r], end = a.ptr[r + 1];
     const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
+    RowPre pre;
+    if (MODE == M_SWEEP && g.lane == 0) {  // issued before the edge loop: overlaps it
+      pre.dq = __ldg(&a.deg[own]);
+      pre.dr = __ldg(&a.deg[r]);
+      pre.szo = __ldg(&a.size[own]);
+    }
     if (MODE == M_MERGE) {
       if (a.size[own] != 1) {
         if (g.lane == 0) a.label_next[r] = own;
@@ -388,34 +472,31 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     }
     const int lg = row_lg(end - beg, LG);  // table prefix sized for this row
     const unsigned mask = (1u << lg) - 1u;
-    for (i64 e = beg + g.lane; e < end; e += G) {
-      int32_t k = __ldg(&a.keys[e]);
-      if (MODE != M_EMIT) k = __ldg(&a.label[k]);
-      tab_insert<true>(keys, vals, mask, lg, k, WT::get(a.w, e));
-    }
+    insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, true, LIST>(a, g.lane, beg, end, keys, vals, mask, lg,
+                                                                            olist, ocnt);
     g.sync();
-    row_epilogue<G, BLOCK, MODE>(g, keys, vals, (i64)1 << lg, r, own, a, acc);
+    const i64 n = LIST ? (i64)(*(volatile int *)ocnt) : ((i64)1 << lg);
+    row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, n, r, own, di, pre, a, acc);
+    g.sync();
+    if (LIST && g.lane == 0) *ocnt = 0;
     g.sync();
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
 
 // ----------------------------------------------------------------- hub path
-// Rows longer than the largest shared-memory bin.  Per hub row h:
-//   k_hub_acc    one CTA per HUB_CHUNK edges: aggregate the chunk in a shared-memory table,
-//                then flush its distinct (key, Σw) into the row's global table; a slot
-//                claimed for the first time is appended to the row's occupied list.
-//   k_hub_fin    nparts CTAs per row, each over a strided share of the occupied list:
-//                score / count / emit, reset the slots, write one partial per CTA.
-//   k_hub_decide one thread per row: combine the partials, decide, reset the row's counters.
+// Rows longer than the largest shared-memory bin.  Per hub row, chunks of HUB_CHUNK
+// edges:
+//   k_hub_acc    one CTA per chunk: aggregate the chunk in a shared-memory table, then
+//                flush its distinct (key, Σw) into the row's global table; the slots this
+//                CTA claims first go to the chunk's own list (no global counter).
+//   k_hub_fin    one CTA per chunk: over the chunk's claimed slots, score / count / emit,
+//                reset them, and write one partial.
+//   k_hub_decide one thread per row: combine the row's partials and decide.
+constexpr i64 HUB_CHUNK = 4096;  // edges per CTA of k_hub_acc (<= 4096 distinct keys)
 constexpr int HUB_ACC_T = 512;
-constexpr int HUB_SM_LG = 13;  // 8192-slot pre-aggregation table (chunk of 4096 edges)
+constexpr int HUB_SM_LG = 13;  // 8192-slot pre-aggregation table for a 4096-edge chunk
 constexpr int HUB_FIN_T = 256;
-constexpr i64 HUB_FIN_PER = 8192;  // occupied entries per fin CTA
-
-struct FinChunk {
-  int32_t h, j, nparts, pad;
-};
 
 struct HubPartial {
   i64 hi;
@@ -425,13 +506,12 @@ struct HubPartial {
 };
 
 struct HubArgs {
-  const FinChunk *fchunks;
-  const i64 *pstart;    // first partial of hub h
-  const int32_t *nparts;
-  int32_t *occ;         // occupied-slot lists (offset toff[h]/2)
-  uint32_t *occ_cnt;    // per hub
+  const i64 *cfirst;    // first chunk of hub h (chunks of a hub are contiguous)
+  const int32_t *ccount;  // chunks of hub h
+  int32_t *clist;       // claimed slots, HUB_CHUNK per chunk
+  int32_t *ccnt;        // claimed count per chunk
   u64 *emit_cur;        // per hub (EMIT output cursor)
-  HubPartial *part;
+  HubPartial *part;     // per chunk
   i64 nhub;
 };
 
@@ -441,39 +521,70 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   constexpr int CAPS = 1 << HUB_SM_LG;
   u64 *svals = (u64 *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)CAPS * sizeof(u64));
+  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPS * 12);
+  __shared__ int scnt, sclaim;
   const Chunk ch = a.chunks[blockIdx.x];
   const int32_t r = a.rows[ch.h];
   if (MODE == M_MERGE) {
     if (a.size[a.label[r]] != 1) return;
   }
   for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
+  if (threadIdx.x == 0) { scnt = 0; sclaim = 0; }
   __syncthreads();
-  for (i64 e = ch.beg + threadIdx.x; e < ch.end; e += HUB_ACC_T) {
-    int32_t k = __ldg(&a.keys[e]);
-    if (MODE != M_EMIT) k = __ldg(&a.label[k]);
-    tab_insert<true>(skeys, svals, CAPS - 1, HUB_SM_LG, k, WT::get(a.w, e));
-  }
+  insert_range<HUB_ACC_T, 8, MODE, WT, true, true>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1, HUB_SM_LG,
+                                                   slist, &scnt);
   __syncthreads();
+  const int n = scnt;
   const int lg = a.tlog[ch.h];
   const i64 off = a.toff[ch.h];
   int32_t *gk = a.tkeys + off;
   u64 *gv = a.tvals + off;
-  int32_t *occ = hb.occ + off / 2;
+  int32_t *mylist = hb.clist + (i64)blockIdx.x * HUB_CHUNK;
   const unsigned mask = (1u << lg) - 1u;
-  for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) {
-    const int32_t k = skeys[s];
-    if (k >= 0) {
-      bool claimed = false;
-      const unsigned slot = tab_insert<false>(gk, gv, mask, lg, k, svals[s], &claimed);
-      if (claimed) occ[atomicAdd(&hb.occ_cnt[ch.h], 1u)] = (int32_t)slot;
+  constexpr int U = 4;
+  for (int t0 = threadIdx.x; t0 < n; t0 += HUB_ACC_T * U) {
+    int32_t k[U];
+    u64 v[U];
+    unsigned h[U];
+    int32_t got[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * HUB_ACC_T;
+      k[u] = -1;
+      v[u] = 0;
+      if (t < n) {
+        const int sl = slist[t];
+        k[u] = skeys[sl];
+        v[u] = svals[sl];
+      }
+      h[u] = hslot(k[u], lg);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) got[u] = k[u] >= 0 ? atomicCAS(&gk[h[u]], -1, k[u]) : k[u];  // first probe
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k[u] < 0) continue;
+      bool claimed = got[u] == -1;
+      if (!claimed && got[u] != k[u]) {
+        while (true) {
+          h[u] = (h[u] + 1) & mask;
+          const int32_t old = atomicCAS(&gk[h[u]], -1, k[u]);
+          if (old == -1) { claimed = true; break; }
+          if (old == k[u]) break;
+        }
+      }
+      atomicAdd(&gv[h[u]], v[u]);
+      if (claimed) mylist[atomicAdd(&sclaim, 1)] = (int32_t)h[u];
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) hb.ccnt[blockIdx.x] = sclaim;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
-  const FinChunk fc = hb.fchunks[blockIdx.x];
-  const int h = fc.h;
+  const Chunk ch = a.chunks[blockIdx.x];
+  const int h = ch.h;
   const int32_t r = a.rows[h];
   const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
   HubPartial P;
@@ -484,70 +595,101 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     const i64 off = a.toff[h];
     int32_t *gk = a.tkeys + off;
     u64 *gv = a.tvals + off;
-    const int32_t *occ = hb.occ + off / 2;
-    const int32_t cnt = (int32_t)hb.occ_cnt[h];
-    const int stride = fc.nparts * HUB_FIN_T;
-    Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
-    u64 eown = 0, n1 = 0, selfw = 0, sumw = 0;
-    int32_t T = -1;
+    const int32_t *lst = hb.clist + (i64)blockIdx.x * HUB_CHUNK;
+    const i64 cnt = hb.ccnt[blockIdx.x];
     const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
-    for (int t = fc.j * HUB_FIN_T + threadIdx.x; t < cnt; t += stride) {
-      const int32_t slot = occ[t];
-      const int32_t k = gk[slot];
-      const u64 v = gv[slot];
-      if (MODE != M_EMIT) { gk[slot] = -1; gv[slot] = 0; }
-      if (MODE == M_SWEEP) {
-        if (k == own) eown = v;
-        else {
-          ++n1;
-          i128 S = (i128)a.twoW * (i128)(i64)v - (i128)di * (i128)__ldg(&a.deg[k]);
-          Cand x;
-          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k;
-          if (cand_better(x, best)) best = x;
+    Grp<HUB_FIN_T, HUB_FIN_T> g;
+    Acc dummy_acc;
+    if (MODE == M_SWEEP) {
+      // partial argmax over this chunk's slots (decision in k_hub_decide)
+      constexpr int U = 4;
+      Cand best;
+      best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+      u64 eown = 0, n1 = 0;
+      int32_t dm = 0;
+      for (i64 t0 = threadIdx.x; t0 < cnt; t0 += (i64)HUB_FIN_T * U) {
+        int32_t sl[U], k[U];
+        u64 v[U];
+        i64 dk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) sl[u] = (t0 + u * HUB_FIN_T < cnt) ? lst[t0 + u * HUB_FIN_T] : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          k[u] = sl[u] >= 0 ? gk[sl[u]] : -1;
+          v[u] = sl[u] >= 0 ? gv[sl[u]] : 0;
         }
-      } else if (MODE == M_MERGE) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (sl[u] >= 0) { gk[sl[u]] = -1; gv[sl[u]] = 0; }
+          dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (k[u] < 0) continue;
+          if (k[u] == own) {
+            eown = v[u];
+          } else {
+            ++n1;
+            i128 S = (i128)a.twoW * (i128)(i64)v[u] - (i128)di * (i128)dk[u];
+            Cand x;
+            x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
+            if (cand_better(x, best)) best = x;
+          }
+        }
+      }
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
+      if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
+    } else if (MODE == M_MERGE) {
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+      u64 n1 = 0, unused = 0;
+      int32_t T = -1;
+      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
+        const int32_t sl = lst[t];
+        const int32_t k = gk[sl];
+        gk[sl] = -1;
+        gv[sl] = 0;
         if (k != own) { ++n1; T = max(T, k); }
-      } else {
+      }
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
+      if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
+    } else {
+      u64 n1 = 0, selfw = 0, sumw = 0;
+      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
+        const int32_t sl = lst[t];
+        const int32_t k = gk[sl];
+        const u64 v = gv[sl];
         sumw += v;
         if (k == r) selfw += v;
         else ++n1;
       }
-    }
-    if (MODE == M_EMIT) {
-      // second pass: write this CTA's entries at a cursor reserved for the CTA
       u64 tot;
-      Grp<HUB_FIN_T, HUB_FIN_T> g;
       const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
       __shared__ u64 sbase;
       if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
       __syncthreads();
       i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
-      for (int t = fc.j * HUB_FIN_T + threadIdx.x; t < cnt; t += stride) {
-        const int32_t slot = occ[t];
-        const int32_t k = gk[slot];
-        const u64 v = gv[slot];
-        gk[slot] = -1;
-        gv[slot] = 0;
+      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
+        const int32_t sl = lst[t];
+        const int32_t k = gk[sl];
+        const u64 v = gv[sl];
+        gk[sl] = -1;
+        gv[sl] = 0;
         if (k != r && a.out_key) {
           a.out_key[o] = k;
           a.out_w[o] = v;
           ++o;
         }
       }
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+      int32_t dm = 0;
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
+      if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
     }
-    Grp<HUB_FIN_T, HUB_FIN_T> g;
-    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, T);
-    Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
-    int32_t dummy = 0;
-    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dummy);
-    if (threadIdx.x == 0) {
-      P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.T = T;
-      P.eown = eown; P.cnt = n1; P.selfw = selfw; P.sumw = sumw;
-    }
+    (void)dummy_acc;
   }
-  if (threadIdx.x == 0) hb.part[hb.pstart[h] + fc.j] = P;
+  if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
 }
 
 template <int MODE>
@@ -561,8 +703,8 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     best.hi = 0; best.lo = 0; best.c = INT32_MAX;
     u64 eown = 0, cnt = 0, selfw = 0, sumw = 0;
     int32_t T = -1;
-    const HubPartial *p = hb.part + hb.pstart[h];
-    for (int j = 0; j < hb.nparts[h]; ++j) {
+    const HubPartial *p = hb.part + hb.cfirst[h];
+    for (int j = 0; j < hb.ccount[h]; ++j) {
       Cand x;
       x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
       if (cand_better(x, best)) best = x;
@@ -593,7 +735,6 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
       if (a.out_self) a.out_self[r] = selfw;
       if (a.out_sum) a.out_sum[r] = sumw;
     }
-    hb.occ_cnt[h] = 0;
     hb.emit_cur[h] = 0;
   }
   if (MODE != M_EMIT) acc.flush(a.counters);

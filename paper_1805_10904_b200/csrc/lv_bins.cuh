@@ -15,7 +15,6 @@ namespace lv {
 constexpr int NSMEM = 8;
 constexpr int NBIN = NSMEM + 1;
 constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 8192};
-constexpr i64 HUB_CHUNK = 4096;  // edges per CTA of k_hub_acc
 
 __device__ __forceinline__ int bin_of(i64 d) {
   if (d <= 0) return 255;
@@ -69,12 +68,9 @@ struct Bins {
   Buf<Chunk> chunks;
   Buf<int32_t> tkeys;
   Buf<u64> tvals;
-  i64 nfin = 0;
-  Buf<FinChunk> fchunks;
-  Buf<i64> pstart;
-  Buf<int32_t> nparts;
-  Buf<int32_t> occ;
-  Buf<uint32_t> occ_cnt;
+  Buf<i64> cfirst;
+  Buf<int32_t> ccount;
+  Buf<int32_t> clist, ccnt;
   Buf<u64> emit_cur;
   Buf<HubPartial> part;
   i64 count(int b) const { return off[b + 1] - off[b]; }
@@ -167,10 +163,9 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
     LV_CUDA(cudaMemcpyAsync(beg.data(), hb.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaMemcpyAsync(len.data(), hl.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
-    std::vector<i64> toff(B.nhub), pstart(B.nhub);
-    std::vector<int32_t> tlog(B.nhub), nparts(B.nhub);
+    std::vector<i64> toff(B.nhub), cfirst(B.nhub);
+    std::vector<int32_t> tlog(B.nhub), ccount(B.nhub);
     std::vector<Chunk> ch;
-    std::vector<FinChunk> fch;
     for (i64 h = 0; h < B.nhub; ++h) {
       const i64 distinct_max = std::min(len[h], universe);
       i64 want = 2 * distinct_max;
@@ -179,6 +174,7 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
       tlog[h] = lg;
       toff[h] = B.tslots;
       B.tslots += (i64)1 << lg;
+      cfirst[h] = (i64)ch.size();
       for (i64 e = 0; e < len[h]; e += HUB_CHUNK) {
         Chunk k;
         k.beg = beg[h] + e;
@@ -187,33 +183,27 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
         k.pad = 0;
         ch.push_back(k);
       }
-      nparts[h] = (int32_t)std::max<i64>(1, cdiv(distinct_max, HUB_FIN_PER));
-      pstart[h] = (i64)fch.size();
-      for (int32_t j = 0; j < nparts[h]; ++j) fch.push_back(FinChunk{(int32_t)h, j, nparts[h], 0});
+      ccount[h] = (int32_t)((i64)ch.size() - cfirst[h]);
     }
     B.nchunks = (i64)ch.size();
-    B.nfin = (i64)fch.size();
     B.toff.alloc(c.A, B.nhub);
     B.tlog.alloc(c.A, B.nhub);
     B.chunks.alloc(c.A, B.nchunks);
     B.tkeys.alloc(c.A, B.tslots);
     B.tvals.alloc(c.A, B.tslots);
-    B.fchunks.alloc(c.A, B.nfin);
-    B.pstart.alloc(c.A, B.nhub);
-    B.nparts.alloc(c.A, B.nhub);
-    B.occ.alloc(c.A, B.tslots / 2);
-    B.occ_cnt.alloc(c.A, B.nhub);
+    B.cfirst.alloc(c.A, B.nhub);
+    B.ccount.alloc(c.A, B.nhub);
+    B.clist.alloc(c.A, B.nchunks * HUB_CHUNK);
+    B.ccnt.alloc(c.A, B.nchunks);
     B.emit_cur.alloc(c.A, B.nhub);
-    B.part.alloc(c.A, B.nfin);
+    B.part.alloc(c.A, B.nchunks);
     LV_CUDA(cudaMemcpyAsync(B.toff.p, toff.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.tlog.p, tlog.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.chunks.p, ch.data(), B.nchunks * sizeof(Chunk), cudaMemcpyHostToDevice, c.s));
-    LV_CUDA(cudaMemcpyAsync(B.fchunks.p, fch.data(), B.nfin * sizeof(FinChunk), cudaMemcpyHostToDevice, c.s));
-    LV_CUDA(cudaMemcpyAsync(B.pstart.p, pstart.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
-    LV_CUDA(cudaMemcpyAsync(B.nparts.p, nparts.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.cfirst.p, cfirst.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.ccount.p, ccount.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemsetAsync(B.tkeys.p, 0xff, B.tslots * sizeof(int32_t), c.s));
     LV_CUDA(cudaMemsetAsync(B.tvals.p, 0, B.tslots * sizeof(u64), c.s));
-    LV_CUDA(cudaMemsetAsync(B.occ_cnt.p, 0, B.nhub * sizeof(uint32_t), c.s));
     LV_CUDA(cudaMemsetAsync(B.emit_cur.p, 0, B.nhub * sizeof(u64), c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));  // host vectors go out of scope
   }
@@ -224,7 +214,7 @@ template <int G, int CAP, int BLOCK, int MODE, class WT>
 void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
   auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT>;
   constexpr int GPB = BLOCK / G;
-  const size_t smem = (size_t)GPB * CAP * (sizeof(u64) + sizeof(int32_t));
+  const size_t smem = smem_bytes<G, CAP, BLOCK>();
   static int occ = -1;
   if (occ < 0) {
     LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -264,15 +254,14 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     a.tlog = B.tlog.p;
     a.chunks = B.chunks.p;
     HubArgs hb;
-    hb.fchunks = B.fchunks.p;
-    hb.pstart = B.pstart.p;
-    hb.nparts = B.nparts.p;
-    hb.occ = B.occ.p;
-    hb.occ_cnt = B.occ_cnt.p;
+    hb.cfirst = B.cfirst.p;
+    hb.ccount = B.ccount.p;
+    hb.clist = B.clist.p;
+    hb.ccnt = B.ccnt.p;
     hb.emit_cur = B.emit_cur.p;
     hb.part = B.part.p;
     hb.nhub = B.nhub;
-    const size_t smem = (size_t)(1 << HUB_SM_LG) * (sizeof(u64) + sizeof(int32_t));
+    const size_t smem = (size_t)(1 << HUB_SM_LG) * (sizeof(u64) + sizeof(int32_t) + sizeof(uint16_t) / 2) + 16;
     static bool attr = false;
     if (!attr) {
       LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -282,7 +271,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     LV_LAUNCH(c, (k_hub_acc<MODE, WT>), (unsigned)B.nchunks, HUB_ACC_T, smem, a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_fin");
-    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nfin, HUB_FIN_T, 0, a, hb);
+    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nchunks, HUB_FIN_T, 0, a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_decide");
     LV_LAUNCH(c, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
