@@ -71,12 +71,7 @@ struct AggArgs {
   u64 *out_self;           // Σ w with key == row id (may be NULL)
   u64 *out_sum;            // Σ w over the row (may be NULL)
   u64 *counters;           // SWEEP/MERGE: [0] I2 [1] moved [2] S2 lo [3] S2 hi [4] cand
-  // hub tables
-  int32_t *tkeys;
-  u64 *tvals;
-  const i64 *toff;         // table offset per hub index
-  const int32_t *tlog;     // log2 capacity per hub index
-  const Chunk *chunks;
+  const Chunk *chunks;     // hub path: HUB_CHUNK-edge chunks of the hub rows
 };
 
 __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
@@ -95,8 +90,10 @@ __device__ __forceinline__ void add_u64_split(u64 *p, u64 v) {
 }
 
 // Open-addressing insert with linear probing; keys -1 = empty.  Returns the slot.
-template <bool SHARED>
-__device__ __forceinline__ unsigned tab_insert(int32_t *keys, u64 *vals, unsigned mask, int lg, int32_t k, u64 v,
+// VT = table value type: uint32_t when the caller has proved every row sum < 2^32
+// (native 32-bit atomics, 9 B per shared slot), else u64.
+template <bool SHARED, class VT>
+__device__ __forceinline__ unsigned tab_insert(int32_t *keys, VT *vals, unsigned mask, int lg, int32_t k, u64 v,
                                                bool *claimed = nullptr) {
   unsigned h = hslot(k, lg);
   while (true) {
@@ -112,9 +109,18 @@ __device__ __forceinline__ unsigned tab_insert(int32_t *keys, u64 *vals, unsigne
     }
     h = (h + 1) & mask;
   }
-  if (SHARED) add_u64_split(&vals[h], v);
-  else atomicAdd(&vals[h], v);
+  if (sizeof(VT) == 4) atomicAdd((uint32_t *)&vals[h], (uint32_t)v);
+  else if (SHARED) add_u64_split((u64 *)&vals[h], v);
+  else atomicAdd((u64 *)&vals[h], v);
   return h;
+}
+
+// Exact move score S = 2W·v − δ·deg (Eq. 4 scaled by 2W², reading D4); all four
+// operands are non-negative, so two 64x64->128 unsigned products suffice.
+__device__ __forceinline__ i128 move_score(i64 twoW, u64 v, i64 di, i64 dk) {
+  const u128 a = ((u128)__umul64hi((u64)twoW, v) << 64) | (u128)((u64)twoW * v);
+  const u128 b = ((u128)__umul64hi((u64)di, (u64)dk) << 64) | (u128)((u64)di * (u64)dk);
+  return (i128)(a - b);
 }
 
 // smallest lg with 2^lg >= 2*d (d >= 1), clamped to [3, LGMAX]
@@ -127,8 +133,8 @@ __device__ __forceinline__ int row_lg(i64 d, int lgmax) {
 // Insert the row's edges [beg, end) into a table, U edges per lane per batch so the
 // col/w loads and then the label gathers of a batch are independent and in flight
 // together (memory-level parallelism; the atomics would otherwise serialise them).
-template <int G, int U, int MODE, class WT, bool SHARED, bool LIST>
-__device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, u64 *vals,
+template <int G, int U, int MODE, class WT, bool SHARED, bool LIST, class VT>
+__device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, VT *vals,
                                              unsigned mask, int lg, uint16_t *olist, int *ocnt) {
   for (i64 e0 = beg + lane; e0 < end; e0 += (i64)G * U) {
     int32_t k[U];
@@ -152,7 +158,7 @@ __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg
     for (int u = 0; u < U; ++u) {
       if (k[u] < 0) continue;
       bool claimed = false;
-      const unsigned sl = tab_insert<SHARED>(keys, vals, mask, lg, k[u], wv[u], LIST ? &claimed : nullptr);
+      const unsigned sl = tab_insert<SHARED, VT>(keys, vals, mask, lg, k[u], wv[u], LIST ? &claimed : nullptr);
       if (LIST && claimed) olist[atomicAdd(ocnt, 1)] = (uint16_t)sl;
     }
   }
@@ -298,8 +304,8 @@ struct RowPre {
 // Visits the row's occupied entries — by scanning slots [0,n) (LIST = false) or through
 // the occupied-slot list olist[0..n) (LIST = true) — resets every slot it reads, and
 // applies the mode's epilogue.  Both EMIT passes visit entries in the same order.
-template <int G, int BLOCK, int MODE, bool LIST, class SlotT>
-__device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, u64 *vals, const SlotT *olist,
+template <int G, int BLOCK, int MODE, bool LIST, class SlotT, class VT>
+__device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, VT *vals, const SlotT *olist,
                                              i64 n, int32_t r, int32_t own, i64 di, const RowPre &pre,
                                              const AggArgs &a, Acc &acc) {
   constexpr int U = G < 32 ? 2 : 4;  // entries per lane per batch: their deg_C gathers overlap
@@ -322,7 +328,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         k[u] = sl[u] >= 0 ? keys[sl[u]] : -1;
         v[u] = 0;
         if (k[u] >= 0) {
-          v[u] = vals[sl[u]];
+          v[u] = (u64)vals[sl[u]];
           keys[sl[u]] = -1;
           vals[sl[u]] = 0;
         }
@@ -336,7 +342,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
           eown = v[u];
         } else {
           ++ncand;
-          i128 S = (i128)a.twoW * (i128)(i64)v[u] - (i128)di * (i128)dk[u];
+          const i128 S = move_score(a.twoW, v[u], di, dk[u]);
           Cand x;
           x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
           if (cand_better(x, best)) best = x;
@@ -384,7 +390,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
       const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
       const int32_t k = keys[sl];
       if (k >= 0) {
-        const u64 v = vals[sl];
+        const u64 v = (u64)vals[sl];
         sumw += v;
         if (k == r) selfw += v;
         else ++c;
@@ -397,7 +403,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
       const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
       const int32_t k = keys[sl];
       if (k >= 0) {
-        const u64 v = vals[sl];
+        const u64 v = (u64)vals[sl];
         keys[sl] = -1;
         vals[sl] = 0;
         if (k != r && a.out_key) {
@@ -424,12 +430,12 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
 // epilogue costs O(distinct keys), not O(capacity).
 template <int CAP>
 constexpr bool has_list() { return CAP >= 256; }
-template <int G, int CAP, int BLOCK>
+template <int G, int CAP, int BLOCK, class VT>
 constexpr size_t smem_bytes() {
-  return (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(u64) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) + 16);
+  return (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(VT) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) + 16);
 }
 
-template <int G, int CAP, int BLOCK, int MODE, class WT>
+template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   constexpr int GPB = BLOCK / G;
   constexpr bool LIST = has_list<CAP>();
@@ -439,14 +445,15 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
                    : (CAP >= 16) ? 4 : 3;
   static_assert((1 << LG) == CAP, "CAP must be a power of two >= 8");
   extern __shared__ __align__(16) unsigned char sm[];
-  u64 *svals = (u64 *)sm;
-  int32_t *skeys = (int32_t *)(sm + (size_t)GPB * CAP * sizeof(u64));
-  uint16_t *slist = (uint16_t *)(sm + (size_t)GPB * CAP * 12);
-  int *scnt = (int *)(sm + (size_t)GPB * CAP * 12 + (LIST ? (size_t)GPB * CAP : 0));
+  constexpr size_t SB = sizeof(VT) + sizeof(int32_t);
+  VT *svals = (VT *)sm;
+  int32_t *skeys = (int32_t *)(sm + (size_t)GPB * CAP * sizeof(VT));
+  uint16_t *slist = (uint16_t *)(sm + (size_t)GPB * CAP * SB);
+  int *scnt = (int *)(sm + (size_t)GPB * CAP * SB + (LIST ? (size_t)GPB * CAP : 0));
   Grp<G, BLOCK> g;
   const int grp = threadIdx.x / G;
   int32_t *keys = skeys + grp * CAP;
-  u64 *vals = svals + grp * CAP;
+  VT *vals = svals + grp * CAP;
   uint16_t *olist = slist + grp * (CAP / 2);
   int *ocnt = scnt + grp;
   Acc acc;
@@ -472,8 +479,8 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     }
     const int lg = row_lg(end - beg, LG);  // table prefix sized for this row
     const unsigned mask = (1u << lg) - 1u;
-    insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, true, LIST>(a, g.lane, beg, end, keys, vals, mask, lg,
-                                                                            olist, ocnt);
+    insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, true, LIST, VT>(a, g.lane, beg, end, keys, vals, mask,
+                                                                                lg, olist, ocnt);
     g.sync();
     const i64 n = LIST ? (i64)(*(volatile int *)ocnt) : ((i64)1 << lg);
     row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, n, r, own, di, pre, a, acc);
@@ -485,18 +492,30 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
 }
 
 // ----------------------------------------------------------------- hub path
-// Rows longer than the largest shared-memory bin.  Per hub row, chunks of HUB_CHUNK
-// edges:
-//   k_hub_acc    one CTA per chunk: aggregate the chunk in a shared-memory table, then
-//                flush its distinct (key, Σw) into the row's global table; the slots this
-//                CTA claims first go to the chunk's own list (no global counter).
-//   k_hub_fin    one CTA per chunk: over the chunk's claimed slots, score / count / emit,
-//                reset them, and write one partial.
+// Rows longer than the largest shared-memory bin (> 4096 entries).  Instead of one
+// global hash table per row (random read-modify-writes over a table far larger than
+// L2), a hub row is radix-partitioned by a second hash of the key:
+//   k_hub_acc    one CTA per HUB_CHUNK-edge chunk: aggregate the chunk in a shared table
+//                (<= 4096 distinct keys), then write its distinct (key, Σw) to the
+//                chunk's pool region grouped by bucket, with the bucket boundaries in
+//                the chunk's segment table.  Sequential writes only.
+//   k_hub_fin    one CTA per (row, bucket): merge that bucket's segments of every chunk
+//                of the row in a shared table (expected <= 1024 distinct keys), then score
+//                / count / emit them and write one partial.
 //   k_hub_decide one thread per row: combine the row's partials and decide.
-constexpr i64 HUB_CHUNK = 4096;  // edges per CTA of k_hub_acc (<= 4096 distinct keys)
+constexpr i64 HUB_CHUNK = 4096;
 constexpr int HUB_ACC_T = 512;
-constexpr int HUB_SM_LG = 13;  // 8192-slot pre-aggregation table for a 4096-edge chunk
+constexpr int HUB_SM_LG = 13;      // chunk table: 8192 slots >= 2 x 4096 distinct (exact bound)
 constexpr int HUB_FIN_T = 256;
+constexpr int HUB_FIN_LG = 12;     // bucket table: 4096 slots
+constexpr int HUB_FIN_MAXD = 2048; // distinct keys allowed per bucket (load <= 0.5); expected <= 1024
+constexpr i64 HUB_BUCKET_TARGET = 1024;
+constexpr int HUB_MAX_BLG = 12;    // <= 4096 buckets per row
+constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
+
+__device__ __forceinline__ unsigned hbucket(int32_t k, int blg) {
+  return blg == 0 ? 0u : (((uint32_t)k * 0x85EBCA77u) >> (32 - blg));
+}
 
 struct HubPartial {
   i64 hi;
@@ -506,188 +525,256 @@ struct HubPartial {
 };
 
 struct HubArgs {
-  const i64 *cfirst;    // first chunk of hub h (chunks of a hub are contiguous)
-  const int32_t *ccount;  // chunks of hub h
-  int32_t *clist;       // claimed slots, HUB_CHUNK per chunk
-  int32_t *ccnt;        // claimed count per chunk
-  u64 *emit_cur;        // per hub (EMIT output cursor)
-  HubPartial *part;     // per chunk
+  const i64 *cfirst;      // per hub: first chunk (chunks of a hub are contiguous)
+  const int32_t *ccount;  // per hub: number of chunks
+  const int32_t *blg;     // per hub: log2 number of buckets
+  const i64 *bfirst;      // per hub: first fin item (one per bucket)
+  const i64 *segoff;      // per chunk: offset of its segment table (nb + 1 entries)
+  int32_t *seg;           // segment boundaries, relative to the chunk's pool region
+  int32_t *pkey;          // pool: chunk c owns [c * HUB_CHUNK, (c+1) * HUB_CHUNK)
+  u64 *pval;
+  const int2 *fitem;      // per fin item: (hub, bucket)
+  HubPartial *part;       // per fin item
+  u64 *emit_cur;          // per hub (EMIT output cursor)
+  int *overflow;          // set if a bucket exceeds HUB_FIN_MAXD distinct keys
   i64 nhub;
 };
 
-template <int MODE, class WT>
+template <class VT>
+constexpr size_t hub_acc_smem() {
+  return (size_t)(1 << HUB_SM_LG) * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t) +
+         (size_t)((1 << HUB_MAX_BLG) + 1) * sizeof(int) + 64;
+}
+template <class VT>
+constexpr size_t hub_fin_smem() {
+  return (size_t)(1 << HUB_FIN_LG) * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_FIN_MAXD * sizeof(uint16_t) +
+         (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
+}
+
+// exclusive scan of cnt[0..n) in shared memory by a CTA of T threads (n <= T * 16)
+template <int T>
+__device__ __forceinline__ int smem_excl_scan(int *cnt, int n) {
+  __shared__ int part[T / 32 + 1];
+  constexpr int PER = 16;
+  int loc[PER];
+  int sum = 0;
+  const int base = threadIdx.x * PER;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = (base + q < n) ? cnt[base + q] : 0;
+    sum += loc[q];
+  }
+  // warp inclusive scan of sum
+  int inc = sum;
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (l >= o) inc += t;
+  }
+  if (l == 31) part[w] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int r = 0;
+    for (int i = 0; i < T / 32; ++i) { const int t = part[i]; part[i] = r; r += t; }
+    part[T / 32] = r;
+  }
+  __syncthreads();
+  int run = part[w] + inc - sum;
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if (base + q < n) { cnt[base + q] = run; run += loc[q]; }
+  const int total = part[T / 32];
+  __syncthreads();
+  return total;
+}
+
+template <int MODE, class WT, class VT>
 __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int CAPS = 1 << HUB_SM_LG;
-  u64 *svals = (u64 *)sm;
-  int32_t *skeys = (int32_t *)(sm + (size_t)CAPS * sizeof(u64));
-  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPS * 12);
-  __shared__ int scnt, sclaim;
+  VT *svals = (VT *)sm;
+  int32_t *skeys = (int32_t *)(sm + (size_t)CAPS * sizeof(VT));
+  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)));
+  int *hist = (int *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t));
+  __shared__ int scnt;
   const Chunk ch = a.chunks[blockIdx.x];
   const int32_t r = a.rows[ch.h];
   if (MODE == M_MERGE) {
     if (a.size[a.label[r]] != 1) return;
   }
   for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
-  if (threadIdx.x == 0) { scnt = 0; sclaim = 0; }
+  const int blg = hb.blg[ch.h];
+  const int nb = 1 << blg;
+  for (int b = threadIdx.x; b <= nb; b += HUB_ACC_T) hist[b] = 0;
+  if (threadIdx.x == 0) scnt = 0;
   __syncthreads();
-  insert_range<HUB_ACC_T, 8, MODE, WT, true, true>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1, HUB_SM_LG,
-                                                   slist, &scnt);
+  insert_range<HUB_ACC_T, 8, MODE, WT, true, true, VT>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1,
+                                                       HUB_SM_LG, slist, &scnt);
   __syncthreads();
   const int n = scnt;
-  const int lg = a.tlog[ch.h];
-  const i64 off = a.toff[ch.h];
-  int32_t *gk = a.tkeys + off;
-  u64 *gv = a.tvals + off;
-  int32_t *mylist = hb.clist + (i64)blockIdx.x * HUB_CHUNK;
-  const unsigned mask = (1u << lg) - 1u;
-  constexpr int U = 4;
-  for (int t0 = threadIdx.x; t0 < n; t0 += HUB_ACC_T * U) {
-    int32_t k[U];
-    u64 v[U];
-    unsigned h[U];
-    int32_t got[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = t0 + u * HUB_ACC_T;
-      k[u] = -1;
-      v[u] = 0;
-      if (t < n) {
-        const int sl = slist[t];
-        k[u] = skeys[sl];
-        v[u] = svals[sl];
-      }
-      h[u] = hslot(k[u], lg);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) got[u] = k[u] >= 0 ? atomicCAS(&gk[h[u]], -1, k[u]) : k[u];  // first probe
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (k[u] < 0) continue;
-      bool claimed = got[u] == -1;
-      if (!claimed && got[u] != k[u]) {
-        while (true) {
-          h[u] = (h[u] + 1) & mask;
-          const int32_t old = atomicCAS(&gk[h[u]], -1, k[u]);
-          if (old == -1) { claimed = true; break; }
-          if (old == k[u]) break;
-        }
-      }
-      atomicAdd(&gv[h[u]], v[u]);
-      if (claimed) mylist[atomicAdd(&sclaim, 1)] = (int32_t)h[u];
-    }
-  }
+  for (int t = threadIdx.x; t < n; t += HUB_ACC_T) atomicAdd(&hist[hbucket(skeys[slist[t]], blg)], 1);
   __syncthreads();
-  if (threadIdx.x == 0) hb.ccnt[blockIdx.x] = sclaim;
+  smem_excl_scan<HUB_ACC_T>(hist, nb);  // hist[b] = start of bucket b
+  int32_t *seg = hb.seg + hb.segoff[blockIdx.x];
+  for (int b = threadIdx.x; b < nb; b += HUB_ACC_T) seg[b] = hist[b];
+  if (threadIdx.x == 0) seg[nb] = n;
+  __syncthreads();
+  const i64 base = (i64)blockIdx.x * HUB_CHUNK;
+  for (int t = threadIdx.x; t < n; t += HUB_ACC_T) {
+    const int sl = slist[t];
+    const int32_t k = skeys[sl];
+    const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
+    hb.pkey[base + pos] = k;
+    hb.pval[base + pos] = (u64)svals[sl];
+  }
 }
 
-template <int MODE>
+template <int MODE, class VT>
 __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
-  const Chunk ch = a.chunks[blockIdx.x];
-  const int h = ch.h;
+  extern __shared__ __align__(16) unsigned char sm[];
+  constexpr int CAPF = 1 << HUB_FIN_LG;
+  VT *svals = (VT *)sm;
+  int32_t *skeys = (int32_t *)(sm + (size_t)CAPF * sizeof(VT));
+  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
+  i64 *tst = (i64 *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_FIN_MAXD * sizeof(uint16_t));
+  int *tlen = (int *)(tst + HUB_FIN_TILE);
+  __shared__ int scnt, sovf;
+  const int2 it = hb.fitem[blockIdx.x];
+  const int h = it.x, b = it.y;
   const int32_t r = a.rows[h];
   const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
   HubPartial P;
   P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1;
   P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
-  const bool skip = (MODE == M_MERGE) && a.size[own] != 1;
-  if (!skip) {
-    const i64 off = a.toff[h];
-    int32_t *gk = a.tkeys + off;
-    u64 *gv = a.tvals + off;
-    const int32_t *lst = hb.clist + (i64)blockIdx.x * HUB_CHUNK;
-    const i64 cnt = hb.ccnt[blockIdx.x];
-    const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
-    Grp<HUB_FIN_T, HUB_FIN_T> g;
-    Acc dummy_acc;
-    if (MODE == M_SWEEP) {
-      // partial argmax over this chunk's slots (decision in k_hub_decide)
-      constexpr int U = 4;
-      Cand best;
-      best.hi = 0; best.lo = 0; best.c = INT32_MAX;
-      u64 eown = 0, n1 = 0;
-      int32_t dm = 0;
-      for (i64 t0 = threadIdx.x; t0 < cnt; t0 += (i64)HUB_FIN_T * U) {
-        int32_t sl[U], k[U];
-        u64 v[U];
-        i64 dk[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) sl[u] = (t0 + u * HUB_FIN_T < cnt) ? lst[t0 + u * HUB_FIN_T] : -1;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          k[u] = sl[u] >= 0 ? gk[sl[u]] : -1;
-          v[u] = sl[u] >= 0 ? gv[sl[u]] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (sl[u] >= 0) { gk[sl[u]] = -1; gv[sl[u]] = 0; }
-          dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (k[u] < 0) continue;
-          if (k[u] == own) {
-            eown = v[u];
-          } else {
-            ++n1;
-            i128 S = (i128)a.twoW * (i128)(i64)v[u] - (i128)di * (i128)dk[u];
-            Cand x;
-            x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
-            if (cand_better(x, best)) best = x;
-          }
-        }
-      }
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
-      if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
-    } else if (MODE == M_MERGE) {
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX;
-      u64 n1 = 0, unused = 0;
-      int32_t T = -1;
-      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
-        const int32_t sl = lst[t];
-        const int32_t k = gk[sl];
-        gk[sl] = -1;
-        gv[sl] = 0;
-        if (k != own) { ++n1; T = max(T, k); }
-      }
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
-      if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
-    } else {
-      u64 n1 = 0, selfw = 0, sumw = 0;
-      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
-        const int32_t sl = lst[t];
-        const int32_t k = gk[sl];
-        const u64 v = gv[sl];
-        sumw += v;
-        if (k == r) selfw += v;
-        else ++n1;
-      }
-      u64 tot;
-      const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
-      __shared__ u64 sbase;
-      if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
-      __syncthreads();
-      i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
-      for (i64 t = threadIdx.x; t < cnt; t += HUB_FIN_T) {
-        const int32_t sl = lst[t];
-        const int32_t k = gk[sl];
-        const u64 v = gv[sl];
-        gk[sl] = -1;
-        gv[sl] = 0;
-        if (k != r && a.out_key) {
-          a.out_key[o] = k;
-          a.out_w[o] = v;
-          ++o;
-        }
-      }
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX;
-      int32_t dm = 0;
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
-      if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
+  if (MODE == M_MERGE && a.size[own] != 1) {
+    if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
+    return;
+  }
+  for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = -1; svals[s] = 0; }
+  if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
+  __syncthreads();
+  const int blg = hb.blg[h];
+  const i64 cf = hb.cfirst[h];
+  const int nch = hb.ccount[h];
+  for (int t0 = 0; t0 < nch; t0 += HUB_FIN_TILE) {
+    const int m = min(HUB_FIN_TILE, nch - t0);
+    for (int j = threadIdx.x; j < m; j += HUB_FIN_T) {
+      const i64 c = cf + t0 + j;
+      const int32_t *seg = hb.seg + hb.segoff[c];
+      const int s0 = seg[b], s1 = seg[b + 1];
+      tlen[j] = s1 - s0;
+      tst[j] = c * HUB_CHUNK + s0;
     }
-    (void)dummy_acc;
+    __syncthreads();
+    const int total = smem_excl_scan<HUB_FIN_T>(tlen, m);  // tlen[j] = prefix
+    for (int t = threadIdx.x; t < total; t += HUB_FIN_T) {
+      int lo = 0, hi = m - 1;  // last j with tlen[j] <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tlen[mid] <= t) lo = mid;
+        else hi = mid - 1;
+      }
+      const i64 e = tst[lo] + (t - tlen[lo]);
+      const int32_t k = hb.pkey[e];
+      const u64 v = hb.pval[e];
+      if (*(volatile int *)&scnt >= HUB_FIN_MAXD - 1) { sovf = 1; continue; }
+      bool claimed = false;
+      const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, HUB_FIN_LG, k, v, &claimed);
+      if (claimed) {
+        const int q = atomicAdd(&scnt, 1);
+        if (q < HUB_FIN_MAXD) slist[q] = (uint16_t)sl;
+        else sovf = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (sovf) {
+    if (threadIdx.x == 0) atomicOr(hb.overflow, 1);
+  }
+  const int n = min(scnt, HUB_FIN_MAXD);
+  Grp<HUB_FIN_T, HUB_FIN_T> g;
+  if (MODE == M_SWEEP) {
+    const i64 di = a.delta[r];
+    constexpr int U = 4;
+    Cand best;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    u64 eown = 0, n1 = 0;
+    int32_t dm = 0;
+    for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
+      int32_t k[U];
+      u64 v[U];
+      i64 dk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * HUB_FIN_T;
+        k[u] = -1;
+        v[u] = 0;
+        if (t < n) {
+          const int sl = slist[t];
+          k[u] = skeys[sl];
+          v[u] = (u64)svals[sl];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k[u] < 0) continue;
+        if (k[u] == own) {
+          eown = v[u];
+        } else {
+          ++n1;
+          const i128 S = move_score(a.twoW, v[u], di, dk[u]);
+          Cand x;
+          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
+          if (cand_better(x, best)) best = x;
+        }
+      }
+    }
+    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
+    if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
+  } else if (MODE == M_MERGE) {
+    Cand none;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    u64 n1 = 0, unused = 0;
+    int32_t T = -1;
+    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
+      const int32_t k = skeys[slist[t]];
+      if (k != own) { ++n1; T = max(T, k); }
+    }
+    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
+    if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
+  } else {
+    u64 n1 = 0, selfw = 0, sumw = 0;
+    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
+      const int sl = slist[t];
+      const int32_t k = skeys[sl];
+      const u64 v = (u64)svals[sl];
+      sumw += v;
+      if (k == r) selfw += v;
+      else ++n1;
+    }
+    u64 tot;
+    const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
+    __shared__ u64 sbase;
+    if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
+    __syncthreads();
+    i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
+    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
+      const int sl = slist[t];
+      const int32_t k = skeys[sl];
+      if (k != r && a.out_key) {
+        a.out_key[o] = k;
+        a.out_w[o] = (u64)svals[sl];
+        ++o;
+      }
+    }
+    Cand none;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    int32_t dm = 0;
+    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
+    if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
   }
   if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
 }
@@ -703,8 +790,9 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     best.hi = 0; best.lo = 0; best.c = INT32_MAX;
     u64 eown = 0, cnt = 0, selfw = 0, sumw = 0;
     int32_t T = -1;
-    const HubPartial *p = hb.part + hb.cfirst[h];
-    for (int j = 0; j < hb.ccount[h]; ++j) {
+    const HubPartial *p = hb.part + hb.bfirst[h];
+    const int np = 1 << hb.blg[h];
+    for (int j = 0; j < np; ++j) {
       Cand x;
       x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
       if (cand_better(x, best)) best = x;

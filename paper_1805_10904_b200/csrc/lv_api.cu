@@ -215,8 +215,9 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int
   a.delta = g.delta.p;
   a.twoW = 2 * g.W;
   a.counters = h->dctr.p;
-  if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, B, a, tm);
-  else launch_agg_wt<M_MERGE>(c, g.wt, B, a, tm);
+  const bool narrow = g.max_delta < ((i64)1 << 32);  // e_{i->C} <= δ_i
+  if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, B, a, tm);
+  else launch_agg_wt<M_MERGE>(c, g.wt, narrow, B, a, tm);
   LV_CUDA(cudaMemcpyAsync(h->hctr, h->dctr.p, NBIN * 8 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
   SweepOut o;

@@ -14,7 +14,7 @@ namespace lv {
 // bin b holds rows of length in (BIN_MAX[b-1], BIN_MAX[b]]; bin NSMEM holds the hubs
 constexpr int NSMEM = 8;
 constexpr int NBIN = NSMEM + 1;
-constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 8192};
+constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 4096};
 
 __device__ __forceinline__ int bin_of(i64 d) {
   if (d <= 0) return 255;
@@ -25,7 +25,7 @@ __device__ __forceinline__ int bin_of(i64 d) {
   if (d <= 128) return 4;
   if (d <= 512) return 5;
   if (d <= 2048) return 6;
-  if (d <= 8192) return 7;
+  if (d <= 4096) return 7;
   return 8;
 }
 
@@ -61,18 +61,15 @@ struct Bins {
   Buf<int32_t> rows;         // active rows grouped by bin (ascending id within a bin)
   i64 off[NBIN + 1] = {0};   // host offsets of each bin in rows
   i64 edges[NBIN] = {0};     // Σ row length per bin
-  // hub tables
-  i64 nhub = 0, nchunks = 0, tslots = 0;
-  Buf<i64> toff;
-  Buf<int32_t> tlog;
+  // hub path (see lv_agg.cuh): chunks, buckets, pool, segment tables, partials
+  i64 nhub = 0, nchunks = 0, nfin = 0, nseg = 0;
   Buf<Chunk> chunks;
-  Buf<int32_t> tkeys;
-  Buf<u64> tvals;
-  Buf<i64> cfirst;
-  Buf<int32_t> ccount;
-  Buf<int32_t> clist, ccnt;
-  Buf<u64> emit_cur;
+  Buf<i64> cfirst, bfirst, segoff;
+  Buf<int32_t> ccount, blg, seg, pkey;
+  Buf<u64> pval, emit_cur;
+  Buf<int2> fitem;
   Buf<HubPartial> part;
+  Buf<int> overflow;
   i64 count(int b) const { return off[b + 1] - off[b]; }
   i64 active() const { return off[NBIN]; }
 };
@@ -155,7 +152,8 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
   // hubs
   B.nhub = cnt[NSMEM];
   B.nchunks = 0;
-  B.tslots = 0;
+  B.nfin = 0;
+  B.nseg = 0;
   if (B.nhub) {
     Buf<i64> hb(c.A, B.nhub), hl(c.A, B.nhub);
     LV_LAUNCH(c, k_gather_len, grid_for(c, B.nhub), 256, 0, B.nhub, B.rows.p + B.off[NSMEM], ptr, hb.p, hl.p);
@@ -163,17 +161,17 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
     LV_CUDA(cudaMemcpyAsync(beg.data(), hb.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaMemcpyAsync(len.data(), hl.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
-    std::vector<i64> toff(B.nhub), cfirst(B.nhub);
-    std::vector<int32_t> tlog(B.nhub), ccount(B.nhub);
+    std::vector<i64> cfirst(B.nhub), bfirst(B.nhub), segoff;
+    std::vector<int32_t> ccount(B.nhub), blg(B.nhub);
     std::vector<Chunk> ch;
+    std::vector<int2> fit;
     for (i64 h = 0; h < B.nhub; ++h) {
       const i64 distinct_max = std::min(len[h], universe);
-      i64 want = 2 * distinct_max;
-      int lg = 5;
-      while (((i64)1 << lg) < want) ++lg;
-      tlog[h] = lg;
-      toff[h] = B.tslots;
-      B.tslots += (i64)1 << lg;
+      int lgb = 0;
+      while (lgb < HUB_MAX_BLG && ((i64)HUB_BUCKET_TARGET << lgb) < distinct_max) ++lgb;
+      LV_REQUIRE(((i64)HUB_BUCKET_TARGET << lgb) >= distinct_max, LV_ERANGE,
+                 "hub row too long for the bucketed hub path (" + std::to_string(len[h]) + " entries)");
+      blg[h] = lgb;
       cfirst[h] = (i64)ch.size();
       for (i64 e = 0; e < len[h]; e += HUB_CHUNK) {
         Chunk k;
@@ -182,39 +180,47 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
         k.h = (int32_t)h;
         k.pad = 0;
         ch.push_back(k);
+        segoff.push_back(B.nseg);
+        B.nseg += ((i64)1 << lgb) + 1;
       }
       ccount[h] = (int32_t)((i64)ch.size() - cfirst[h]);
+      bfirst[h] = (i64)fit.size();
+      for (int b = 0; b < (1 << lgb); ++b) fit.push_back(make_int2((int)h, b));
     }
     B.nchunks = (i64)ch.size();
-    B.toff.alloc(c.A, B.nhub);
-    B.tlog.alloc(c.A, B.nhub);
+    B.nfin = (i64)fit.size();
     B.chunks.alloc(c.A, B.nchunks);
-    B.tkeys.alloc(c.A, B.tslots);
-    B.tvals.alloc(c.A, B.tslots);
     B.cfirst.alloc(c.A, B.nhub);
     B.ccount.alloc(c.A, B.nhub);
-    B.clist.alloc(c.A, B.nchunks * HUB_CHUNK);
-    B.ccnt.alloc(c.A, B.nchunks);
+    B.blg.alloc(c.A, B.nhub);
+    B.bfirst.alloc(c.A, B.nhub);
+    B.segoff.alloc(c.A, B.nchunks);
+    B.seg.alloc(c.A, B.nseg);
+    B.pkey.alloc(c.A, B.nchunks * HUB_CHUNK);
+    B.pval.alloc(c.A, B.nchunks * HUB_CHUNK);
+    B.fitem.alloc(c.A, B.nfin);
+    B.part.alloc(c.A, B.nfin);
     B.emit_cur.alloc(c.A, B.nhub);
-    B.part.alloc(c.A, B.nchunks);
-    LV_CUDA(cudaMemcpyAsync(B.toff.p, toff.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
-    LV_CUDA(cudaMemcpyAsync(B.tlog.p, tlog.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+    B.overflow.alloc(c.A, 1);
     LV_CUDA(cudaMemcpyAsync(B.chunks.p, ch.data(), B.nchunks * sizeof(Chunk), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.cfirst.p, cfirst.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(B.ccount.p, ccount.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
-    LV_CUDA(cudaMemsetAsync(B.tkeys.p, 0xff, B.tslots * sizeof(int32_t), c.s));
-    LV_CUDA(cudaMemsetAsync(B.tvals.p, 0, B.tslots * sizeof(u64), c.s));
+    LV_CUDA(cudaMemcpyAsync(B.blg.p, blg.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.bfirst.p, bfirst.data(), B.nhub * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.segoff.p, segoff.data(), B.nchunks * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+    LV_CUDA(cudaMemcpyAsync(B.fitem.p, fit.data(), B.nfin * sizeof(int2), cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemsetAsync(B.emit_cur.p, 0, B.nhub * sizeof(u64), c.s));
+    LV_CUDA(cudaMemsetAsync(B.overflow.p, 0, sizeof(int), c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));  // host vectors go out of scope
   }
 }
 
 // ----------------------------------------------------------------- launch
-template <int G, int CAP, int BLOCK, int MODE, class WT>
+template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
-  auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT>;
+  auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT, VT>;
   constexpr int GPB = BLOCK / G;
-  const size_t smem = smem_bytes<G, CAP, BLOCK>();
+  const size_t smem = smem_bytes<G, CAP, BLOCK, VT>();
   static int occ = -1;
   if (occ < 0) {
     LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -232,10 +238,11 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
 
 static const char *BIN_NAME[NBIN] = {"agg_g4_c8",      "agg_g8_c16",      "agg_g16_c32",
                                      "agg_g32_c64",    "agg_g32_c256",    "agg_blk128_c1024",
-                                     "agg_blk256_c4096", "agg_blk512_c16384", "agg_hub"};
+                                     "agg_blk256_c4096", "agg_blk512_c8192", "agg_hub"};
 
-// One pass of MODE over every bin of B.  `a` carries the common arguments.
-template <int MODE, class WT>
+// One pass of MODE over every bin of B.  `a` carries the common arguments.  VT is the
+// shared-table value type (uint32_t only when every row sum is known to be < 2^32).
+template <int MODE, class WT, class VT>
 void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   static const char *MN[3] = {"sweep", "merge", "emit"};
   u64 *ctr = a.counters;  // NBIN slots of 8 counters (one per bin) or NULL
@@ -248,50 +255,66 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   // hub path first (longest rows), then the big bins, then the small ones
   if (B.nhub) {
     set(NSMEM);
-    a.tkeys = B.tkeys.p;
-    a.tvals = B.tvals.p;
-    a.toff = B.toff.p;
-    a.tlog = B.tlog.p;
     a.chunks = B.chunks.p;
     HubArgs hb;
     hb.cfirst = B.cfirst.p;
     hb.ccount = B.ccount.p;
-    hb.clist = B.clist.p;
-    hb.ccnt = B.ccnt.p;
-    hb.emit_cur = B.emit_cur.p;
+    hb.blg = B.blg.p;
+    hb.bfirst = B.bfirst.p;
+    hb.segoff = B.segoff.p;
+    hb.seg = B.seg.p;
+    hb.pkey = B.pkey.p;
+    hb.pval = B.pval.p;
+    hb.fitem = B.fitem.p;
     hb.part = B.part.p;
+    hb.emit_cur = B.emit_cur.p;
+    hb.overflow = B.overflow.p;
     hb.nhub = B.nhub;
-    const size_t smem = (size_t)(1 << HUB_SM_LG) * (sizeof(u64) + sizeof(int32_t) + sizeof(uint16_t) / 2) + 16;
     static bool attr = false;
     if (!attr) {
-      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)hub_acc_smem<VT>()));
+      LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)hub_fin_smem<VT>()));
       attr = true;
     }
     if (tm) tm->begin(c.s, pre + "hub_acc");
-    LV_LAUNCH(c, (k_hub_acc<MODE, WT>), (unsigned)B.nchunks, HUB_ACC_T, smem, a, hb);
+    LV_LAUNCH(c, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, hub_acc_smem<VT>(), a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_fin");
-    LV_LAUNCH(c, (k_hub_fin<MODE>), (unsigned)B.nchunks, HUB_FIN_T, 0, a, hb);
+    LV_LAUNCH(c, (k_hub_fin<MODE, VT>), (unsigned)B.nfin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_decide");
     LV_LAUNCH(c, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
     if (tm) tm->end(c.s);
   }
-  if (B.count(7)) { set(7); launch_bin<512, 16384, 512, MODE, WT>(c, tm, a, (pre + BIN_NAME[7]).c_str()); }
-  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[6]).c_str()); }
-  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT>(c, tm, a, (pre + BIN_NAME[5]).c_str()); }
-  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[4]).c_str()); }
-  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[3]).c_str()); }
-  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[2]).c_str()); }
-  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[1]).c_str()); }
-  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT>(c, tm, a, (pre + BIN_NAME[0]).c_str()); }
+  if (B.nhub) {  // a bucket beyond HUB_FIN_MAXD distinct keys would have been dropped
+    int ovf = 0;
+    LV_CUDA(cudaMemcpyAsync(&ovf, B.overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    LV_REQUIRE(ovf == 0, LV_ECUDA, "hub bucket overflow (a hash bucket exceeded its table)");
+  }
+  if (B.count(7)) { set(7); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[7]).c_str()); }
+  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str()); }
+  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str()); }
+  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[4]).c_str()); }
+  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str()); }
+  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str()); }
+  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str()); }
+  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[0]).c_str()); }
 }
 
 template <int MODE>
-void launch_agg_wt(Ctx &c, int wt, const Bins &B, const AggArgs &a, KTimer *tm = nullptr) {
-  if (wt == WT_NONE) launch_agg<MODE, WNone>(c, B, a, tm);
-  else if (wt == WT_U32) launch_agg<MODE, WU32>(c, B, a, tm);
-  else launch_agg<MODE, WU64>(c, B, a, tm);
+void launch_agg_wt(Ctx &c, int wt, bool narrow, const Bins &B, const AggArgs &a, KTimer *tm = nullptr) {
+  if (narrow) {
+    if (wt == WT_NONE) launch_agg<MODE, WNone, uint32_t>(c, B, a, tm);
+    else if (wt == WT_U32) launch_agg<MODE, WU32, uint32_t>(c, B, a, tm);
+    else launch_agg<MODE, WU64, uint32_t>(c, B, a, tm);
+  } else {
+    if (wt == WT_NONE) launch_agg<MODE, WNone, u64>(c, B, a, tm);
+    else if (wt == WT_U32) launch_agg<MODE, WU32, u64>(c, B, a, tm);
+    else launch_agg<MODE, WU64, u64>(c, B, a, tm);
+  }
 }
 
 }  // namespace lv

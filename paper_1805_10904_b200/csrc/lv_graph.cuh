@@ -21,6 +21,7 @@ namespace lv {
 
 struct DGraph {
   i64 n = 0, nnz = 0, W = 0;
+  i64 max_delta = 0;      // max δ_i: bounds every row sum (u32 tables iff < 2^32)
   int wt = WT_NONE;
   Buf<i64> row_ptr;       // n+1
   Buf<int32_t> col;       // nnz
@@ -39,7 +40,7 @@ template <class R>
 __global__ void __launch_bounds__(256) k_coo_count(i64 m, i64 n, const int32_t *__restrict__ src,
                                                    const int32_t *__restrict__ dst, const void *w, i64 *loop,
                                                    uint32_t *cnt, u64 *Wacc, int *err) {
-  u64 s = 0;
+  u64 s = 0, mx = 0;
   for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
     const int32_t u = src[k], v = dst[k];
     const i64 wk = R::get(w, k);
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(256) k_coo_count(i64 m, i64 n, const int32_t *
       continue;
     }
     s += (u64)wk;
+    mx = (u64)wk > mx ? (u64)wk : mx;
     if (u == v) {
       atomicAdd((u64 *)&loop[u], (u64)wk);
     } else {
@@ -55,6 +57,12 @@ __global__ void __launch_bounds__(256) k_coo_count(i64 m, i64 n, const int32_t *
       atomicAdd(&cnt[v], 1u);
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = y > mx ? y : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(Wacc + 2, mx);
   s = block_sum_u64<256>(s);
   if (threadIdx.x == 0 && s) atomicAdd(Wacc, s);
 }
@@ -158,6 +166,16 @@ struct I64Arr {
   __device__ __forceinline__ i64 operator()(i64 i) const { return a[i]; }
 };
 
+inline i64 max_of(Ctx &c, const i64 *p, i64 n) {
+  Buf<u64> t(c.A, 1);
+  LV_CUDA(cudaMemsetAsync(t.p, 0, sizeof(u64), c.s));
+  LV_LAUNCH(c, k_max_u64<I64Arr>, grid_for(c, n), 256, 0, I64Arr{p}, n, t.p);
+  u64 v;
+  LV_CUDA(cudaMemcpyAsync(&v, t.p, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  return (i64)v;
+}
+
 inline i64 d2h_i64(Ctx &c, const i64 *p) {
   i64 v;
   LV_CUDA(cudaMemcpyAsync(&v, p, sizeof(i64), cudaMemcpyDeviceToHost, c.s));
@@ -175,8 +193,8 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   LV_CUDA(cudaMemsetAsync(g.loop.p, 0, n * sizeof(i64), c.s));
   Buf<uint32_t> cnt(c.A, n);
   LV_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(uint32_t), c.s));
-  Buf<u64> scal(c.A, 2);  // [0] W, [1] err
-  LV_CUDA(cudaMemsetAsync(scal.p, 0, 2 * sizeof(u64), c.s));
+  Buf<u64> scal(c.A, 3);  // [0] W, [1] err, [2] max weight
+  LV_CUDA(cudaMemsetAsync(scal.p, 0, 3 * sizeof(u64), c.s));
   int *err = (int *)(scal.p + 1);
   const unsigned gm = grid_for(c, m);
   if (m > 0) {
@@ -184,8 +202,8 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
     else if (in_wt == LV_W_I32) LV_LAUNCH(c, k_coo_count<RI32>, gm, 256, 0, m, n, src, dst, w, g.loop.p, cnt.p, scal.p, err);
     else LV_LAUNCH(c, k_coo_count<RI64>, gm, 256, 0, m, n, src, dst, w, g.loop.p, cnt.p, scal.p, err);
   }
-  u64 hs[2];
-  LV_CUDA(cudaMemcpyAsync(hs, scal.p, 2 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  u64 hs[3];
+  LV_CUDA(cudaMemcpyAsync(hs, scal.p, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
   LV_REQUIRE(((int)hs[1]) == 0, LV_EGRAPH, "vertex id outside [0,n) or weight <= 0 (P:L43: positive weights)");
   g.W = (i64)hs[0];
@@ -222,7 +240,9 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   a.out_w = tw.p;
   a.out_cnt = ocnt.p;
   a.out_sum = osum.p;
-  launch_agg_wt<M_EMIT>(c, raw_wt, B, a);
+  // every shared table / hub chunk holds <= 4096 entries of weight <= max w
+  const bool narrow = hs[2] < ((u64)1 << 20);
+  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);
   rcol.release();
   rw.release();
   g.row_ptr.alloc(c.A, n + 1);
@@ -234,7 +254,7 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   g.w.alloc(c.A, g.nnz * (i64)wbytes(g.wt) + 8);
   copy_rows(c, g.wt, B, rptr.p, ocnt.p, g.row_ptr.p, tk.p, tw.p, g.col.p, g.w.p);
   LV_LAUNCH(c, k_delta, grid_for(c, n), 256, 0, n, osum.p, g.loop.p, g.delta.p);
-  LV_CUDA(cudaStreamSynchronize(c.s));
+  g.max_delta = max_of(c, g.delta.p, n);
 }
 
 // ------------------------------------------------------------------ renumber
@@ -406,7 +426,9 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   a.out_w = tw.p;
   a.out_cnt = ocnt.p;
   a.out_self = oself.p;
-  launch_agg_wt<M_EMIT>(c, g.wt, CB, a);
+  // a community's row sum is at most its deg_C
+  const i64 maxdeg = max_of(c, ndelta.p, k);
+  launch_agg_wt<M_EMIT>(c, g.wt, maxdeg < ((i64)1 << 32), CB, a);
   pk.release();
   pw.release();
   h.n = k;
@@ -421,6 +443,7 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   h.loop.alloc(c.A, k);
   LV_LAUNCH(c, k_finish_loop, grid_for(c, k), 256, 0, k, nloop.p, oself.p, h.loop.p);
   h.delta = std::move(ndelta);
+  h.max_delta = maxdeg;
   LV_CUDA(cudaStreamSynchronize(c.s));
 }
 

@@ -130,6 +130,22 @@ __global__ void __launch_bounds__(256) k_sum_u64(F f, i64 n, u64 *out) {
   if (threadIdx.x == 0 && s) atomicAdd(out, s);
 }
 
+// Device-wide max of non-negative values into *out (u64).
+template <typename F>
+__global__ void __launch_bounds__(256) k_max_u64(F f, i64 n, u64 *out) {
+  u64 m = 0;
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    const u64 x = (u64)f(i);
+    m = x > m ? x : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 // Device-wide sum of squares of non-negative i64 values (exact 128-bit) into out[0]=lo,out[1]=hi.
 template <typename F>
 __global__ void __launch_bounds__(256) k_sumsq_u128(F f, i64 n, u64 *out) {
