@@ -8,8 +8,9 @@
 //                 S_own = 2W·e_{i->own} − δ_i·(deg_own − δ_i)
 //             (Eq. 4 scaled by 2W², reading D4), best = argmax by (S desc, label asc)
 //             (Eq. 5 + generalized minimum label, D7), move iff
-//             S(best) > S_own (D6), singlet rule (D8).  It also emits
-//             e_{i->own} and deg[i]² for the exact Eq. 3 numerators of the snapshot.
+//             S(best) > S_own (D6), singlet rule (D8).  A move is recorded
+//             in the next-state deg/size.  It also emits e_{i->own} and deg[i]²
+//             for the exact Eq. 3 numerators of the snapshot.
 //   M_MERGE : isolated-node merge (D14): a singlet whose neighbours lie in
 //             exactly one community T moves to T (singlet rule applies).
 //   M_EMIT  : distinct (key, Σw) per row, for duplicate merging in "Neighbor
@@ -19,10 +20,9 @@
 //
 // Rows are binned by length (P:L438 motivates grouping by degree): bins of
 // G ∈ {4,8,16,32} lanes per row with per-group shared-memory open-addressing tables,
-// block-per-row bins with block-wide shared tables up to 16384 slots (192 KB), and a
-// hub path for longer rows: a global-memory table per row filled by many CTAs
-// (k_hub_acc), then one CTA per row runs the epilogue (k_hub_fin).  All sums are exact
-// integers, so the result is independent of insertion order and schedule.
+// CTA-per-row bins with shared tables up to 8192 slots, and a hub path for rows longer
+// than 4096 (radix-partitioned by a second key hash; see "hub path").  All sums are
+// exact integers, so the result is independent of insertion order and schedule.
 #pragma once
 #include "lv_common.cuh"
 
@@ -35,16 +35,19 @@ struct WNone {
   static constexpr int id = WT_NONE;
   static constexpr int bytes = 0;
   __device__ __forceinline__ static u64 get(const void *, i64) { return 1ull; }
+  __device__ __forceinline__ static u64 get(const void *, i64, u64) { return 1ull; }
 };
 struct WU32 {
   static constexpr int id = WT_U32;
   static constexpr int bytes = 4;
   __device__ __forceinline__ static u64 get(const void *w, i64 e) { return __ldg((const uint32_t *)w + e); }
+  __device__ __forceinline__ static u64 get(const void *w, i64 e, u64 pol) { return ld_stream((const uint32_t *)w + e, pol); }
 };
 struct WU64 {
   static constexpr int id = WT_U64;
   static constexpr int bytes = 8;
   __device__ __forceinline__ static u64 get(const void *w, i64 e) { return __ldg((const u64 *)w + e); }
+  __device__ __forceinline__ static u64 get(const void *w, i64 e, u64 pol) { return ld_stream((const u64 *)w + e, pol); }
 };
 
 struct Chunk {
@@ -60,8 +63,10 @@ struct AggArgs {
   const void *w;           // weights (WT)
   const int32_t *label;    // snapshot labels C
   int32_t *label_next;     // decisions
-  const i64 *deg;          // deg_C, indexed by label
-  const int32_t *size;     // |C|, indexed by label
+  const i64 *deg;          // deg_C, indexed by label (snapshot)
+  const int32_t *size;     // |C|, indexed by label (snapshot)
+  i64 *deg_next;           // SWEEP/MERGE: copy of deg receiving this pass's moves
+  int32_t *size_next;      //   (P:L291 remove/insert; exact int64 atomics, order-free)
   const i64 *delta;        // δ_i
   i64 twoW;                // 2W
   const i64 *out_base;     // EMIT: output offset of row r (NULL -> ptr)
@@ -72,6 +77,7 @@ struct AggArgs {
   u64 *out_sum;            // Σ w over the row (may be NULL)
   u64 *counters;           // SWEEP/MERGE: [0] I2 [1] moved [2] S2 lo [3] S2 hi [4] cand
   const Chunk *chunks;     // hub path: HUB_CHUNK-edge chunks of the hub rows
+  int hint;                // bit0: evict_first on streams; bit1: evict_last on gathers
 };
 
 __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
@@ -136,6 +142,7 @@ __device__ __forceinline__ int row_lg(i64 d, int lgmax) {
 template <int G, int U, int MODE, class WT, bool SHARED, bool LIST, class VT>
 __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, VT *vals,
                                              unsigned mask, int lg, uint16_t *olist, int *ocnt) {
+  const u64 pf = l2_policy_first(), pl = l2_policy_last();
   for (i64 e0 = beg + lane; e0 < end; e0 += (i64)G * U) {
     int32_t k[U];
     u64 wv[U];
@@ -145,14 +152,19 @@ __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg
       k[u] = -1;
       wv[u] = 0;
       if (e < end) {
-        k[u] = __ldg(&a.keys[e]);
-        wv[u] = WT::get(a.w, e);
+        if (a.hint & 1) {
+          k[u] = ld_stream(&a.keys[e], pf);
+          wv[u] = WT::get(a.w, e, pf);
+        } else {
+          k[u] = __ldg(&a.keys[e]);
+          wv[u] = WT::get(a.w, e);
+        }
       }
     }
     if (MODE != 2 /* M_EMIT */) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (k[u] >= 0) k[u] = __ldg(&a.label[k[u]]);
+        if (k[u] >= 0) k[u] = (a.hint & 2) ? ld_keep(&a.label[k[u]], pl) : __ldg(&a.label[k[u]]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -294,6 +306,15 @@ struct Acc {
   }
 };
 
+// Record a move own -> tgt of vertex r (weighted degree di) in the next-state deg/size
+// ("remove ... from the old community ... insert ... into the new").
+__device__ __forceinline__ void record_move(const AggArgs &a, int32_t own, int32_t tgt, i64 di) {
+  atomicAdd((u64 *)&a.deg_next[own], (u64)(-di));
+  atomicAdd((u64 *)&a.deg_next[tgt], (u64)di);
+  atomicSub(&a.size_next[own], 1);
+  atomicAdd(&a.size_next[tgt], 1);
+}
+
 // ----------------------------------------------------------------- row epilogue
 // Per-row scalars the group's lane 0 prefetches before the insertion loop (SWEEP).
 struct RowPre {
@@ -334,7 +355,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
+      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (k[u] < 0) continue;
@@ -358,6 +379,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         if (pre.szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule
       }
       a.label_next[r] = tgt;
+      if (tgt != own) record_move(a, own, tgt, di);
       acc.moved += (tgt != own);
       acc.i2 += eown;
       acc.cand += ncand;
@@ -382,6 +404,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
       int32_t tgt = own;
       if (cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
       a.label_next[r] = tgt;
+      if (tgt != own) record_move(a, own, tgt, a.delta[r]);
       acc.moved += (tgt != own);
     }
   } else {  // M_EMIT
@@ -500,16 +523,16 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
 //                chunk's pool region grouped by bucket, with the bucket boundaries in
 //                the chunk's segment table.  Sequential writes only.
 //   k_hub_fin    one CTA per (row, bucket): merge that bucket's segments of every chunk
-//                of the row in a shared table (expected <= 1024 distinct keys), then score
+//                of the row in a shared table (expected <= 2048 distinct keys), then score
 //                / count / emit them and write one partial.
 //   k_hub_decide one thread per row: combine the row's partials and decide.
 constexpr i64 HUB_CHUNK = 4096;
 constexpr int HUB_ACC_T = 512;
 constexpr int HUB_SM_LG = 13;      // chunk table: 8192 slots >= 2 x 4096 distinct (exact bound)
 constexpr int HUB_FIN_T = 256;
-constexpr int HUB_FIN_LG = 12;     // bucket table: 4096 slots
-constexpr int HUB_FIN_MAXD = 2048; // distinct keys allowed per bucket (load <= 0.5); expected <= 1024
-constexpr i64 HUB_BUCKET_TARGET = 1024;
+constexpr int HUB_FIN_LG = 13;     // bucket table: 8192 slots
+constexpr int HUB_FIN_MAXD = 4096; // distinct keys allowed per bucket (load <= 0.5); expected <= 2048
+constexpr i64 HUB_BUCKET_TARGET = 2048;
 constexpr int HUB_MAX_BLG = 12;    // <= 4096 buckets per row
 constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
 
@@ -717,7 +740,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? __ldg(&a.deg[k[u]]) : 0;
+      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (k[u] < 0) continue;
@@ -809,6 +832,7 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
         if (a.size[own] == 1 && a.size[best.c] == 1 && best.c > own) tgt = own;
       }
       a.label_next[r] = tgt;
+      if (tgt != own) record_move(a, own, tgt, di);
       acc.moved += (tgt != own);
       acc.i2 += eown;
       acc.cand += cnt;
@@ -817,6 +841,7 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
       int32_t tgt = own;
       if (a.size[own] == 1 && cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
       a.label_next[r] = tgt;
+      if (tgt != own) record_move(a, own, tgt, a.delta[r]);
       acc.moved += (tgt != own);
     } else {
       a.out_cnt[r] = (i64)cnt;
@@ -826,25 +851,6 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     hb.emit_cur[h] = 0;
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
-}
-
-// ----------------------------------------------------------------- commit
-// deg_C / |C| update for every vertex whose decision differs from the snapshot
-// ("remove ... insert ... atomicSub/atomicAdd").  Exact int64 atomics: the
-// result is independent of their order.
-__global__ void __launch_bounds__(256) k_commit(i64 n, const int32_t *__restrict__ cur,
-                                                const int32_t *__restrict__ nxt, const i64 *__restrict__ delta,
-                                                i64 *deg, int32_t *size) {
-  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
-    const int32_t a = cur[i], b = nxt[i];
-    if (a != b) {
-      const i64 d = delta[i];
-      atomicAdd((u64 *)&deg[a], (u64)(-d));
-      atomicAdd((u64 *)&deg[b], (u64)d);
-      atomicSub(&size[a], 1);
-      atomicAdd(&size[b], 1);
-    }
-  }
 }
 
 }  // namespace lv

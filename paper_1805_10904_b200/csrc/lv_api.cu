@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -164,6 +165,9 @@ struct louvain_ctx {
   u64 *hctr = nullptr;         // pinned host copy of the sweep counters
   Buf<u64> dctr;               // NBIN x 8 device counters
   std::unique_ptr<Bins> vb0;   // level-0 vertex bins (step-level API)
+  int l2mode = 1;              // LV_L2MODE: bit0 evict_first streams (default), bit1 evict_last
+                               // gathers, bit2 persisting L2 window on the snapshot labels
+  size_t l2win = 0;
   ~louvain_ctx() {
     levels.clear();
     final_part.release();
@@ -178,11 +182,13 @@ struct louvain_ctx {
 
 namespace {
 
-// Per-level community state: double-buffered labels (snapshot / next), deg_C, |C|.
+// Per-level community state, double-buffered (snapshot `cur` / next `cur ^ 1`): labels,
+// deg_C and |C|.  A pass writes decisions and their deg/size deltas into the next
+// buffers; commit = flip `cur`; a dropped pass is simply never flipped in.
 struct State {
   Buf<int32_t> lab[2];
-  Buf<i64> deg;
-  Buf<int32_t> size;
+  Buf<i64> deg[2];
+  Buf<int32_t> size[2];
   int cur = 0;
 };
 
@@ -210,11 +216,28 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int
   a.w = g.w.p;
   a.label = st.lab[st.cur].p;
   a.label_next = st.lab[st.cur ^ 1].p;
-  a.deg = st.deg.p;
-  a.size = st.size.p;
+  a.deg = st.deg[st.cur].p;
+  a.size = st.size[st.cur].p;
+  a.deg_next = st.deg[st.cur ^ 1].p;
+  a.size_next = st.size[st.cur ^ 1].p;
+  if (tm) tm->begin(c.s, "next_state_copy");
+  LV_CUDA(cudaMemcpyAsync(a.deg_next, a.deg, (size_t)g.n * sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
+  LV_CUDA(cudaMemcpyAsync(a.size_next, a.size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+  if (tm) tm->end(c.s);
   a.delta = g.delta.p;
   a.twoW = 2 * g.W;
   a.counters = h->dctr.p;
+  a.hint = h->l2mode & 3;
+  if (h->l2mode & 4) {  // keep the snapshot labels resident in the persisting L2 carve-out
+    cudaStreamAttrValue v;
+    memset(&v, 0, sizeof(v));
+    v.accessPolicyWindow.base_ptr = (void *)st.lab[st.cur].p;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)g.n * sizeof(int32_t), (size_t)h->l2win);
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    LV_CUDA(cudaStreamSetAttribute(c.s, cudaStreamAttributeAccessPolicyWindow, &v));
+  }
   const bool narrow = g.max_delta < ((i64)1 << 32);  // e_{i->C} <= δ_i
   if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, B, a, tm);
   else launch_agg_wt<M_MERGE>(c, g.wt, narrow, B, a, tm);
@@ -246,7 +269,7 @@ double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, c
   if (nm == "sweep:hub_acc") return (double)B.edges[NSMEM] * (8.0 + wb);
   if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand;
   if (nm == "sweep:hub_decide") return 56.0 * (double)B.count(NSMEM);
-  if (nm == "commit") return 8.0 * (double)g.n + 56.0 * (double)moved;
+  if (nm == "next_state_copy") return 24.0 * (double)g.n;  // deg + size: read + write
   return 0.0;
 }
 
@@ -260,23 +283,18 @@ void account(Prof &P, KTimer &tm, const Bins &B, const DGraph &g, const std::vec
   tm.clear();
 }
 
-void commit(louvain_ctx *h, const DGraph &g, State &st, KTimer *tm = nullptr) {
-  Ctx &c = h->c;
-  if (tm) tm->begin(c.s, "commit");
-  LV_LAUNCH(c, k_commit, grid_for(c, g.n), 256, 0, g.n, st.lab[st.cur].p, st.lab[st.cur ^ 1].p, g.delta.p, st.deg.p,
-            st.size.p);
-  if (tm) tm->end(c.s);
-  st.cur ^= 1;
-}
+void commit(louvain_ctx *, const DGraph &, State &st, KTimer * = nullptr) { st.cur ^= 1; }
 
 void init_state(louvain_ctx *h, const DGraph &g, State &st) {
   Ctx &c = h->c;
-  st.lab[0].alloc(c.A, g.n);
-  st.lab[1].alloc(c.A, g.n);
-  st.deg.alloc(c.A, g.n);
-  st.size.alloc(c.A, g.n);
+  for (int b = 0; b < 2; ++b) {
+    st.lab[b].alloc(c.A, g.n);
+    st.deg[b].alloc(c.A, g.n);
+    st.size[b].alloc(c.A, g.n);
+  }
   st.cur = 0;
-  LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg.p, st.size.p, g.delta.p);
+  LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg[0].p, st.size[0].p,
+            g.delta.p);
 }
 
 // Level constants: Σ loop and Σ_{inactive} δ² (labels of vertices without neighbours
@@ -383,7 +401,7 @@ void run_impl(louvain_ctx *h) {
     double t2 = now_ms();
     rec->labels.alloc(c.A, g->n);
     Buf<i64> ndelta;
-    const i64 k = renumber(c, g->n, st.lab[st.cur].p, st.size.p, st.deg.p, rec->labels.p, ndelta);
+    const i64 k = renumber(c, g->n, st.lab[st.cur].p, st.size[st.cur].p, st.deg[st.cur].p, rec->labels.p, ndelta);
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t3 = now_ms();
     st = State();
@@ -485,6 +503,14 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
     h->c.A.ctx = cfg.alloc_ctx;
     h->c.A.s = h->c.s;
     LV_CUDA(cudaMallocHost((void **)&h->hctr, NBIN * 8 * sizeof(u64)));
+    if (const char *e = getenv("LV_L2MODE")) h->l2mode = atoi(e);
+    if (h->l2mode & 4) {
+      int maxp = 0, maxw = 0;
+      LV_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, cfg.device));
+      LV_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, cfg.device));
+      LV_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
+      h->l2win = std::min<size_t>((size_t)maxp, (size_t)maxw);
+    }
     h->dctr.alloc(h->c.A, NBIN * 8);
     // input to device
     const int32_t *src = gr->src, *dst = gr->dst;
@@ -595,18 +621,20 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     const i64 n = g.n;
     Bins &B = vbins0(h);
     State st;
-    st.lab[0].alloc(c.A, n);
-    st.lab[1].alloc(c.A, n);
-    st.deg.alloc(c.A, n);
-    st.size.alloc(c.A, n);
+    for (int b = 0; b < 2; ++b) {
+      st.lab[b].alloc(c.A, n);
+      st.deg[b].alloc(c.A, n);
+      st.size[b].alloc(c.A, n);
+    }
     LV_CUDA(cudaMemcpyAsync(st.lab[0].p, labels_in, n * sizeof(int32_t),
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(st.lab[1].p, st.lab[0].p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
-    LV_CUDA(cudaMemsetAsync(st.deg.p, 0, n * sizeof(i64), c.s));
-    LV_CUDA(cudaMemsetAsync(st.size.p, 0, n * sizeof(int32_t), c.s));
+    LV_CUDA(cudaMemsetAsync(st.deg[0].p, 0, n * sizeof(i64), c.s));
+    LV_CUDA(cudaMemsetAsync(st.size[0].p, 0, n * sizeof(int32_t), c.s));
     Buf<int> err(c.A, 1);
     LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
-    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg.p, st.size.p, err.p);
+    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg[0].p, st.size[0].p,
+              err.p);
     int herr = 0;
     LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
@@ -624,7 +652,7 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     level_consts(h, g, lsum, s2i);
     Buf<u64> t(c.A, 2);
     LV_CUDA(cudaMemsetAsync(t.p, 0, 2 * sizeof(u64), c.s));
-    LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, n), 256, 0, DegArr{st.deg.p}, n, t.p);
+    LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, n), 256, 0, DegArr{st.deg[0].p}, n, t.p);
     u64 ht[2];
     LV_CUDA(cudaMemcpyAsync(ht, t.p, sizeof(ht), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaMemcpyAsync(labels_out, st.lab[1].p, n * sizeof(int32_t),

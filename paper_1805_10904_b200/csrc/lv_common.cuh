@@ -159,4 +159,48 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v) {
   return t;
 }
 
+// ---- L2 eviction-priority hints (PTX createpolicy + ld.global.L2::cache_hint).
+// Streams read once (row_ptr, col, w) are marked evict_first so they do not push the
+// randomly gathered arrays (labels, deg_C) out of the 126 MB L2; those are evict_last.
+__device__ __forceinline__ u64 l2_policy_first() {
+  u64 p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ u64 l2_policy_last() {
+  u64 p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *a, u64 pol) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *a, u64 pol) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ u64 ld_stream(const u64 *a, u64 pol) {
+  u64 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ i64 ld_stream(const i64 *a, u64 pol) {
+  i64 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_keep(const int32_t *a, u64 pol) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ i64 ld_keep(const i64 *a, u64 pol) {
+  i64 v;
+  asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 }  // namespace lv
