@@ -533,7 +533,7 @@ constexpr int HUB_FIN_T = 256;
 constexpr int HUB_FIN_LG = 13;     // bucket table: 8192 slots
 constexpr int HUB_FIN_MAXD = 4096; // distinct keys allowed per bucket (load <= 0.5); expected <= 2048
 constexpr i64 HUB_BUCKET_TARGET = 2048;
-constexpr int HUB_MAX_BLG = 12;    // <= 4096 buckets per row
+constexpr int HUB_MAX_BLG = 15;    // <= 32768 buckets per row (histogram sized per launch)
 constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
 
 __device__ __forceinline__ unsigned hbucket(int32_t k, int blg) {
@@ -564,9 +564,9 @@ struct HubArgs {
 };
 
 template <class VT>
-constexpr size_t hub_acc_smem() {
+constexpr size_t hub_acc_smem(int max_blg) {
   return (size_t)(1 << HUB_SM_LG) * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t) +
-         (size_t)((1 << HUB_MAX_BLG) + 1) * sizeof(int) + 64;
+         (size_t)((1 << max_blg) + 1) * sizeof(int) + 64;
 }
 template <class VT>
 constexpr size_t hub_fin_smem() {
@@ -574,20 +574,15 @@ constexpr size_t hub_fin_smem() {
          (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
 }
 
-// exclusive scan of cnt[0..n) in shared memory by a CTA of T threads (n <= T * 16)
+// exclusive scan of cnt[0..n) in shared memory by a CTA of T threads; returns the total
 template <int T>
 __device__ __forceinline__ int smem_excl_scan(int *cnt, int n) {
   __shared__ int part[T / 32 + 1];
-  constexpr int PER = 16;
-  int loc[PER];
+  const int per = (n + T - 1) / T;
+  const int base = threadIdx.x * per;
+  const int lim = min(base + per, n);
   int sum = 0;
-  const int base = threadIdx.x * PER;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    loc[q] = (base + q < n) ? cnt[base + q] : 0;
-    sum += loc[q];
-  }
-  // warp inclusive scan of sum
+  for (int q = base; q < lim; ++q) sum += cnt[q];
   int inc = sum;
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -604,9 +599,11 @@ __device__ __forceinline__ int smem_excl_scan(int *cnt, int n) {
   }
   __syncthreads();
   int run = part[w] + inc - sum;
-#pragma unroll
-  for (int q = 0; q < PER; ++q)
-    if (base + q < n) { cnt[base + q] = run; run += loc[q]; }
+  for (int q = base; q < lim; ++q) {
+    const int v = cnt[q];
+    cnt[q] = run;
+    run += v;
+  }
   const int total = part[T / 32];
   __syncthreads();
   return total;

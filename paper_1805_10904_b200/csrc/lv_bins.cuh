@@ -3,6 +3,7 @@
 // emit) over all bins.  Bins are rebuilt once per level and reused by every sweep.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -63,6 +64,7 @@ struct Bins {
   i64 edges[NBIN] = {0};     // Σ row length per bin
   // hub path (see lv_agg.cuh): chunks, buckets, pool, segment tables, partials
   i64 nhub = 0, nchunks = 0, nfin = 0, nseg = 0;
+  int max_blg = 0;
   Buf<Chunk> chunks;
   Buf<i64> cfirst, bfirst, segoff;
   Buf<int32_t> ccount, blg, seg, pkey;
@@ -165,13 +167,17 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
     std::vector<int32_t> ccount(B.nhub), blg(B.nhub);
     std::vector<Chunk> ch;
     std::vector<int2> fit;
+    // LV_HUB_BUCKET_TARGET (tests only) shrinks the bucket target to exercise many buckets
+    static const i64 target = getenv("LV_HUB_BUCKET_TARGET") ? atoll(getenv("LV_HUB_BUCKET_TARGET"))
+                                                              : HUB_BUCKET_TARGET;
     for (i64 h = 0; h < B.nhub; ++h) {
       const i64 distinct_max = std::min(len[h], universe);
       int lgb = 0;
-      while (lgb < HUB_MAX_BLG && ((i64)HUB_BUCKET_TARGET << lgb) < distinct_max) ++lgb;
-      LV_REQUIRE(((i64)HUB_BUCKET_TARGET << lgb) >= distinct_max, LV_ERANGE,
+      while (lgb < HUB_MAX_BLG && (target << lgb) < distinct_max) ++lgb;
+      LV_REQUIRE((target << lgb) >= distinct_max, LV_ERANGE,
                  "hub row too long for the bucketed hub path (" + std::to_string(len[h]) + " entries)");
       blg[h] = lgb;
+      B.max_blg = std::max(B.max_blg, lgb);
       cfirst[h] = (i64)ch.size();
       for (i64 e = 0; e < len[h]; e += HUB_CHUNK) {
         Chunk k;
@@ -270,16 +276,20 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.emit_cur = B.emit_cur.p;
     hb.overflow = B.overflow.p;
     hb.nhub = B.nhub;
-    static bool attr = false;
-    if (!attr) {
-      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)hub_acc_smem<VT>()));
+    const size_t acc_smem = hub_acc_smem<VT>(B.max_blg);
+    static size_t attr_acc = 0;
+    static bool attr_fin = false;
+    if (acc_smem > attr_acc) {
+      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
+      attr_acc = acc_smem;
+    }
+    if (!attr_fin) {
       LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)hub_fin_smem<VT>()));
-      attr = true;
+      attr_fin = true;
     }
     if (tm) tm->begin(c.s, pre + "hub_acc");
-    LV_LAUNCH(c, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, hub_acc_smem<VT>(), a, hb);
+    LV_LAUNCH(c, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, acc_smem, a, hb);
     if (tm) tm->end(c.s);
     if (tm) tm->begin(c.s, pre + "hub_fin");
     LV_LAUNCH(c, (k_hub_fin<MODE, VT>), (unsigned)B.nfin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);

@@ -14,7 +14,7 @@ from paper_1805_10904_b200 import Louvain, LouvainError, inputs
 pytestmark = pytest.mark.gpu
 
 
-def _canon(rp, col, w):
+def _canon_slow(rp, col, w):
     """Rows sorted by column (row order within a row is not specified by the method)."""
     col2, w2 = col.copy(), w.copy()
     for i in range(len(rp) - 1):
@@ -244,3 +244,105 @@ def test_device_inputs_and_repeat_determinism():
         out = torch.empty(r.n, dtype=torch.int32, device="cuda")
         b.partition(out=out)
         assert np.array_equal(out.cpu().numpy(), pa)
+
+
+def test_many_hub_buckets_parity():
+    """Hub rows split into thousands of hash buckets (the path giant communities take in
+    contraction): a subprocess with a tiny bucket target must match the oracle."""
+    import subprocess
+    import sys
+    import os
+
+    code = (
+        "import numpy as np, oracle\n"
+        "from test_gpu_parity import _star_plus\n"
+        "from paper_1805_10904_b200 import Louvain, inputs\n"
+        "for r in (_star_plus(seed=3, hub_deg=30000), inputs.rmat(15, 16, seed=9)):\n"
+        "    og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)\n"
+        "    want = oracle.run(og)\n"
+        "    with Louvain(r.n, r.src, r.dst, r.w) as g:\n"
+        "        g.run()\n"
+        "        assert [g.level_stats(l)[0] for l in range(g.num_levels)] == want.sweeps\n"
+        "        assert np.array_equal(g.partition(-1), want.final)\n"
+        "        assert g.modularity() == want.final_q\n"
+        "print('ok')\n")
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LV_HUB_BUCKET_TARGET="4",
+               PYTHONPATH=os.pathsep.join([here, os.path.dirname(here), os.environ.get("PYTHONPATH", "")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def _q_numpy_exact(r, part):
+    """Eq. 3 recomputed from the raw COO records in numpy (independent of both sides):
+    I2 = Σ over records inside one community of 2w (a loop counts 2w, reading D2),
+    S2 = Σ_C (Σ_{i∈C} δ_i)², Q = (2W·I2 − S2) / 4W²; returned as an exact Fraction."""
+    from fractions import Fraction
+
+    w = np.ones(r.m, np.int64) if r.w is None else r.w.astype(np.int64)
+    W = int(w.sum())
+    delta = np.bincount(r.src, weights=w, minlength=r.n).astype(np.int64) + \
+        np.bincount(r.dst, weights=w, minlength=r.n).astype(np.int64)
+    same = part[r.src] == part[r.dst]
+    I2 = 2 * int(w[same].sum())
+    degc = np.bincount(part, weights=delta, minlength=int(part.max()) + 1).astype(np.int64)
+    S2 = sum(int(x) * int(x) for x in degc[degc > 0])
+    return Fraction(2 * W * I2 - S2, 4 * W * W), W, delta
+
+
+@pytest.mark.slow
+def test_full_size_rmat24_properties():
+    """C4 at full size in the bench configuration (R-MAT scale 24): the oracle cannot run
+    here in seconds, so check what holds at any size — W and δ against the raw records,
+    the final Q against an independent exact Eq. 3 evaluation, dense renumbered levels,
+    the dendrogram composition, and bit-identical repeated runs."""
+    r = inputs.rmat(24, 16, seed=4)
+    with Louvain(r.n, r.src, r.dst, r.w) as g:
+        csr = g.csr()
+        g.run()
+        final = g.partition(-1)
+        q = g.modularity(-1)
+        levels = [g.partition(l) for l in range(g.num_levels)]
+        g.run()
+        assert np.array_equal(g.partition(-1), final)
+    qx, W, delta = _q_numpy_exact(r, final)
+    assert csr["W"] == W
+    assert np.array_equal(csr["delta"], delta)
+    assert int(csr["delta"].sum()) == 2 * W
+    assert abs(q - float(qx)) <= 1e-12 * max(1.0, abs(float(qx)))
+    comp = levels[0].copy()
+    for l, lab in enumerate(levels):
+        assert lab.min() == 0 and len(np.unique(lab)) == lab.max() + 1  # dense (D18)
+        if l:
+            comp = lab[comp]
+    assert np.array_equal(comp, final)
+
+
+@pytest.mark.slow
+def test_rmat20_full_run_parity():
+    """R-MAT scale 20 (4M vertices, 33M directed edges): every level identical to the
+    oracle (the largest size the single-threaded oracle finishes in ~2 minutes)."""
+    r = inputs.rmat(20, 16, seed=4)
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    want = oracle.run(og)
+    with Louvain(r.n, r.src, r.dst, r.w) as g:
+        g.run()
+        assert [g.level_stats(l)[0] for l in range(g.num_levels)] == want.sweeps
+        for l in range(g.num_levels):
+            assert np.array_equal(g.partition(l), want.levels[l])
+            assert g.modularity(l) == want.q[l]
+
+
+@pytest.mark.slow
+def test_sbm_full_size_ground_truth():
+    """C2 at full size (1M vertices, 1000 planted blocks, μ = 0.3): the final partition
+    equals the planted one and Q equals its exact Eq. 3 value."""
+    r = inputs.sbm()
+    with Louvain(r.n, r.src, r.dst) as g:
+        g.run()
+        final = g.partition(-1)
+        q = g.modularity(-1)
+    pairs = set(zip(final.tolist(), r.truth.tolist()))
+    assert len(pairs) == 1000 == len(set(final.tolist()))
+    qx, _, _ = _q_numpy_exact(r, final)
+    assert abs(q - float(qx)) <= 1e-12
