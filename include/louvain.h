@@ -183,6 +183,12 @@ louvain_status louvain_nccl_init(const uint8_t id[128], int32_t world, int32_t r
                                  void **comm_out);
 louvain_status louvain_nccl_destroy(void *comm);
 
+/* Sweep sharding (host helper, no GPU): contiguous edge-balanced vertex ranges of a CSR,
+ * bounds[p] = first vertex v with row_ptr[v] >= p*nnz/world (bounds[0] = 0,
+ * bounds[world] = n), the same rule the library applies on the device per level.
+ * row_ptr: host, n+1 entries; bounds: host, world+1 entries. */
+louvain_status louvain_shard_bounds(const int64_t *row_ptr, int64_t n, int32_t world, int64_t *bounds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ EXPORTS = [
     "louvain_config_default", "louvain_create", "louvain_run", "louvain_num_levels", "louvain_level_size",
     "louvain_get_partition", "louvain_modularity", "louvain_level_stats", "louvain_run_stats", "louvain_sweep",
     "louvain_time_sweeps", "louvain_profile_json", "louvain_get_csr", "louvain_contract", "louvain_last_error", "louvain_destroy",
-    "louvain_nccl_unique_id", "louvain_nccl_init", "louvain_nccl_destroy",
+    "louvain_nccl_unique_id", "louvain_nccl_init", "louvain_nccl_destroy", "louvain_shard_bounds",
 ]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -102,6 +102,7 @@ def load() -> C.CDLL:
         "louvain_nccl_unique_id": ([P], C.c_int),
         "louvain_nccl_init": ([P, i32, i32, i32, C.POINTER(P)], C.c_int),
         "louvain_nccl_destroy": ([P], C.c_int),
+        "louvain_shard_bounds": ([P, i64, i32, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -308,7 +308,10 @@ struct Acc {
 
 // Record a move own -> tgt of vertex r (weighted degree di) in the next-state deg/size
 // ("remove ... from the old community ... insert ... into the new").
+// (In the sweep-sharded mode deg_next is NULL: every rank applies all moves after the
+// label exchange instead, see k_apply_moves.)
 __device__ __forceinline__ void record_move(const AggArgs &a, int32_t own, int32_t tgt, i64 di) {
+  if (!a.deg_next) return;
   atomicAdd((u64 *)&a.deg_next[own], (u64)(-di));
   atomicAdd((u64 *)&a.deg_next[tgt], (u64)di);
   atomicSub(&a.size_next[own], 1);
@@ -848,6 +851,23 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     hb.emit_cur[h] = 0;
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
+}
+
+// Apply every move cur -> nxt to the next-state deg/size (sweep-sharded mode: run
+// identically on every rank after the label exchange; exact atomics, order-free).
+__global__ void __launch_bounds__(256) k_apply_moves(i64 n, const int32_t *__restrict__ cur,
+                                                     const int32_t *__restrict__ nxt, const i64 *__restrict__ delta,
+                                                     i64 *deg_next, int32_t *size_next) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    const int32_t a = cur[i], b = nxt[i];
+    if (a != b) {
+      const i64 d = delta[i];
+      atomicAdd((u64 *)&deg_next[a], (u64)(-d));
+      atomicAdd((u64 *)&deg_next[b], (u64)d);
+      atomicSub(&size_next[a], 1);
+      atomicAdd(&size_next[b], 1);
+    }
+  }
 }
 
 }  // namespace lv

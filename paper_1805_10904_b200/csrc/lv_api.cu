@@ -30,6 +30,35 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// ---- NCCL, loaded at run time (dlopen) so the library loads on hosts without it.
+typedef int (*nccl_bcast_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*nccl_group_fn)();
+constexpr int NCCL_INT32 = 2, NCCL_UINT64 = 5;
+
+void *nccl_handle() {
+  static void *lib = nullptr;
+  if (!lib) {
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names)
+      if ((lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+  }
+  return lib;
+}
+template <class F>
+F nccl_sym(const char *name) {
+  void *lib = nccl_handle();
+  LV_REQUIRE(lib != nullptr, LV_ENCCL, "libnccl.so.2 not found");
+  F f = (F)dlsym(lib, name);
+  LV_REQUIRE(f != nullptr, LV_ENCCL, std::string("NCCL symbol missing: ") + name);
+  return f;
+}
+#define LV_NCCL(x)                                                                      \
+  do {                                                                                  \
+    int r_ = (x);                                                                       \
+    LV_REQUIRE(r_ == 0, LV_ENCCL, std::string(#x) + " failed with ncclResult " + std::to_string(r_)); \
+  } while (0)
+
 // D22 (refined): pinned int128 -> fp64 on the magnitude.
 double d128(i128 x) {
   const bool neg = x < 0;
@@ -165,6 +194,10 @@ struct louvain_ctx {
   u64 *hctr = nullptr;         // pinned host copy of the sweep counters
   Buf<u64> dctr;               // NBIN x 8 device counters
   std::unique_ptr<Bins> vb0;   // level-0 vertex bins (step-level API)
+  // sweep-sharded mode: nccl_comm given, or LV_SHARD_SIM=P virtual ranks
+  bool shard = false;
+  int world = 1, rank = 0, sim = 0;
+  void *comm = nullptr;
   int l2mode = 1;              // LV_L2MODE: bit0 evict_first streams (default), bit1 evict_last
                                // gathers, bit2 persisting L2 window on the snapshot labels
   size_t l2win = 0;
@@ -176,6 +209,7 @@ struct louvain_ctx {
     g0 = DGraph();
     if (c.s) cudaStreamSynchronize(c.s);
     if (hctr) cudaFreeHost(hctr);
+    c.free_side();
     if (own_stream && c.s) cudaStreamDestroy(c.s);
   }
 };
@@ -204,11 +238,64 @@ struct SweepOut {
 double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<struct SweepOut> &pb,
                         u64 moved);
 
-// Run one pass of MODE over the bins of g (snapshot st.lab[cur] -> st.lab[cur^1]).
-SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int mode, KTimer *tm = nullptr,
+// The sweep work of one level: the bins this process sweeps.  Unsharded: one Bins over
+// all rows.  Sweep-sharded: contiguous edge-balanced vertex ranges (bounds); with NCCL a
+// process sweeps its own range, with LV_SHARD_SIM all P virtual ranks run in-process.
+struct Plan {
+  std::vector<std::unique_ptr<Bins>> own;
+  std::vector<const Bins *> parts;
+  std::vector<i64> bounds;
+  bool sharded = false, nccl = false;
+  std::unique_ptr<Bins> full;  // all rows (contraction), built on demand when sharded
+  const Bins &all(Ctx &c, const DGraph &g) {
+    if (!sharded) return *parts[0];
+    if (!full) {
+      full = std::make_unique<Bins>();
+      build_bins(c, g.row_ptr.p, g.n, g.n, *full);
+    }
+    return *full;
+  }
+};
+
+Plan make_plan(louvain_ctx *h, const DGraph &g) {
+  Ctx &c = h->c;
+  Plan P;
+  if (!h->shard) {
+    P.own.push_back(std::make_unique<Bins>());
+    build_bins(c, g.row_ptr.p, g.n, g.n, *P.own[0]);
+    P.parts.push_back(P.own[0].get());
+    return P;
+  }
+  P.sharded = true;
+  P.nccl = h->comm != nullptr;
+  const int W = h->world;
+  Buf<i64> db(c.A, W + 1);
+  LV_LAUNCH(c, k_shard_bounds, 1, 1024, 0, g.n, g.row_ptr.p, W, db.p);
+  P.bounds.resize(W + 1);
+  LV_CUDA(cudaMemcpyAsync(P.bounds.data(), db.p, (W + 1) * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  for (int p = 0; p < W; ++p) {
+    if (P.nccl && p != h->rank) continue;
+    P.own.push_back(std::make_unique<Bins>());
+    build_bins(c, g.row_ptr.p, g.n, g.n, *P.own.back(), P.bounds[p], P.bounds[p + 1]);
+    P.parts.push_back(P.own.back().get());
+  }
+  return P;
+}
+
+Plan plan_of(Bins &B) {  // unsharded view of existing bins (step-level entry points)
+  Plan P;
+  P.parts.push_back(&B);
+  return P;
+}
+
+// Run one pass of MODE (snapshot st.lab[cur] -> st.lab[cur^1], deg/size -> next buffers).
+SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int mode, KTimer *tm = nullptr,
                   std::vector<SweepOut> *per_bin = nullptr) {
   Ctx &c = h->c;
-  LV_CUDA(cudaMemsetAsync(h->dctr.p, 0, NBIN * 8 * sizeof(u64), c.s));
+  const int nloc = (int)P.parts.size();
+  const size_t SLOT = (size_t)NBIN * 8;
+  LV_CUDA(cudaMemsetAsync(h->dctr.p, 0, (size_t)nloc * SLOT * sizeof(u64), c.s));
   AggArgs a;
   memset(&a, 0, sizeof(a));
   a.ptr = g.row_ptr.p;
@@ -218,15 +305,17 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int
   a.label_next = st.lab[st.cur ^ 1].p;
   a.deg = st.deg[st.cur].p;
   a.size = st.size[st.cur].p;
-  a.deg_next = st.deg[st.cur ^ 1].p;
-  a.size_next = st.size[st.cur ^ 1].p;
+  i64 *deg_next = st.deg[st.cur ^ 1].p;
+  int32_t *size_next = st.size[st.cur ^ 1].p;
+  a.deg_next = P.sharded ? nullptr : deg_next;  // sharded: all moves applied after the exchange
+  a.size_next = P.sharded ? nullptr : size_next;
+  if (tm && mode == M_SWEEP) tm->begin(c.s, "sweep_pass");
   if (tm) tm->begin(c.s, "next_state_copy");
-  LV_CUDA(cudaMemcpyAsync(a.deg_next, a.deg, (size_t)g.n * sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
-  LV_CUDA(cudaMemcpyAsync(a.size_next, a.size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+  LV_CUDA(cudaMemcpyAsync(deg_next, a.deg, (size_t)g.n * sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
+  LV_CUDA(cudaMemcpyAsync(size_next, a.size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
   if (tm) tm->end(c.s);
   a.delta = g.delta.p;
   a.twoW = 2 * g.W;
-  a.counters = h->dctr.p;
   a.hint = h->l2mode & 3;
   if (h->l2mode & 4) {  // keep the snapshot labels resident in the persisting L2 carve-out
     cudaStreamAttrValue v;
@@ -239,23 +328,49 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, int
     LV_CUDA(cudaStreamSetAttribute(c.s, cudaStreamAttributeAccessPolicyWindow, &v));
   }
   const bool narrow = g.max_delta < ((i64)1 << 32);  // e_{i->C} <= δ_i
-  if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, B, a, tm);
-  else launch_agg_wt<M_MERGE>(c, g.wt, narrow, B, a, tm);
-  LV_CUDA(cudaMemcpyAsync(h->hctr, h->dctr.p, NBIN * 8 * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  for (int j = 0; j < nloc; ++j) {
+    a.counters = h->dctr.p + (size_t)j * SLOT;
+    if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, *P.parts[j], a, tm);
+    else launch_agg_wt<M_MERGE>(c, g.wt, narrow, *P.parts[j], a, tm);
+  }
+  int nsum = nloc;
+  const u64 *src = h->dctr.p;
+  if (P.nccl) {  // exchange: every rank's new labels, and every rank's counters
+    auto bcast = nccl_sym<nccl_bcast_fn>("ncclBroadcast");
+    auto gather = nccl_sym<nccl_allgather_fn>("ncclAllGather");
+    auto gstart = nccl_sym<nccl_group_fn>("ncclGroupStart");
+    auto gend = nccl_sym<nccl_group_fn>("ncclGroupEnd");
+    LV_NCCL(gstart());
+    for (int p = 0; p < h->world; ++p) {
+      const i64 lo = P.bounds[p], cnt = P.bounds[p + 1] - P.bounds[p];
+      if (cnt > 0)
+        LV_NCCL(bcast(a.label_next + lo, a.label_next + lo, (size_t)cnt, NCCL_INT32, p, h->comm, c.s));
+    }
+    LV_NCCL(gend());
+    LV_NCCL(gather(h->dctr.p, h->dctr.p + SLOT, SLOT, NCCL_UINT64, h->comm, c.s));
+    nsum = h->world;
+    src = h->dctr.p + SLOT;
+  }
+  if (P.sharded)  // identical on every rank: apply all moves to the next-state deg/size
+    LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, a.label, a.label_next, g.delta.p, deg_next, size_next);
+  if (tm && mode == M_SWEEP) tm->end(c.s);
+  LV_CUDA(cudaMemcpyAsync(h->hctr, src, (size_t)nsum * SLOT * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
   SweepOut o;
   for (int b = 0; b < NBIN; ++b) {
-    const u64 *x = h->hctr + 8 * b;
-    SweepOut p;
-    p.i2 = x[0];
-    p.moved = x[1];
-    p.s2 = ((u128)x[3] << 64) | x[2];
-    p.cand = x[4];
-    o.i2 += p.i2;
-    o.moved += p.moved;
-    o.s2 += p.s2;
-    o.cand += p.cand;
-    if (per_bin) per_bin->push_back(p);
+    SweepOut pbin;
+    for (int j = 0; j < nsum; ++j) {
+      const u64 *x = h->hctr + (size_t)j * SLOT + 8 * b;
+      pbin.i2 += x[0];
+      pbin.moved += x[1];
+      pbin.s2 += ((u128)x[3] << 64) | x[2];
+      pbin.cand += x[4];
+    }
+    o.i2 += pbin.i2;
+    o.moved += pbin.moved;
+    o.s2 += pbin.s2;
+    o.cand += pbin.cand;
+    if (per_bin) per_bin->push_back(pbin);
   }
   return o;
 }
@@ -270,14 +385,22 @@ double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, c
   if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand;
   if (nm == "sweep:hub_decide") return 56.0 * (double)B.count(NSMEM);
   if (nm == "next_state_copy") return 24.0 * (double)g.n;  // deg + size: read + write
+  if (nm == "sweep_pass") {  // the whole pass: every bin + hub path + next-state copy
+    double t = 24.0 * (double)g.n;
+    for (int b = 0; b < NSMEM; ++b) t += kernel_alg_bytes(std::string("sweep:") + BIN_NAME[b], B, g, pb, moved);
+    t += kernel_alg_bytes("sweep:hub_acc", B, g, pb, moved) + kernel_alg_bytes("sweep:hub_fin", B, g, pb, moved) +
+         kernel_alg_bytes("sweep:hub_decide", B, g, pb, moved);
+    return t;
+  }
   return 0.0;
 }
 
 void account(Prof &P, KTimer &tm, const Bins &B, const DGraph &g, const std::vector<SweepOut> &pb, u64 moved) {
   for (size_t k = 0; k < tm.names.size(); ++k) {
     float kt = 0;
-    LV_CUDA(cudaEventSynchronize(tm.ev[2 * k + 1]));
-    LV_CUDA(cudaEventElapsedTime(&kt, tm.ev[2 * k], tm.ev[2 * k + 1]));
+    if (!tm.t1[k]) continue;
+    LV_CUDA(cudaEventSynchronize(tm.t1[k]));
+    LV_CUDA(cudaEventElapsedTime(&kt, tm.t0[k], tm.t1[k]));
     P.add(tm.names[k], kt, kernel_alg_bytes(tm.names[k], B, g, pb, moved));
   }
   tm.clear();
@@ -314,17 +437,18 @@ void level_consts(louvain_ctx *h, const DGraph &g, u64 &lsum, u128 &s2_inact) {
 }
 
 // Algorithm 1 for one level.  Returns the number of committed sweeps.
-int32_t one_level(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, double theta) {
+int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, double theta) {
   const louvain_config &cfg = h->cfg;
   if (cfg.max_sweeps <= 0) return 0;
   u64 lsum;
   u128 s2i;
   level_consts(h, g, lsum, s2i);
-  const bool prof = cfg.profile != 0;
+  const bool prof = cfg.profile != 0 && !P.sharded;
+  const Bins &B = *P.parts[0];
   KTimer tm;
   tm.on = prof;
   std::vector<SweepOut> pb;
-  SweepOut o = run_pass(h, g, B, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);
+  SweepOut o = run_pass(h, g, P, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);
   h->edge_visits += g.nnz;
   commit(h, g, st, prof ? &tm : nullptr);
   if (prof) account(h->prof, tm, B, g, pb, o.moved);
@@ -334,7 +458,7 @@ int32_t one_level(louvain_ctx *h, const DGraph &g, const Bins &B, State &st, dou
   double Qp = 0.0;
   for (int32_t s = 2; s <= cfg.max_sweeps; ++s) {
     pb.clear();
-    o = run_pass(h, g, B, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);  // tentative sweep s
+    o = run_pass(h, g, P, st, M_SWEEP, prof ? &tm : nullptr, prof ? &pb : nullptr);  // tentative sweep s
     h->edge_visits += g.nnz;
     const i128 I2 = (i128)o.i2 + (i128)2 * (i128)lsum;  // numerators of state s-1
     const i128 S2 = (i128)(o.s2 + s2i);
@@ -388,13 +512,12 @@ void run_impl(louvain_ctx *h) {
     double t0 = now_ms();
     State st;
     init_state(h, *g, st);
-    Bins B;
-    build_bins(c, g->row_ptr.p, g->n, g->n, B);
+    Plan P = make_plan(h, *g);
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t1 = now_ms();
-    rec->sweeps = one_level(h, *g, B, st, theta);
+    rec->sweeps = one_level(h, *g, P, st, theta);
     if (cfg.merge_isolated) {
-      run_pass(h, *g, B, st, M_MERGE);
+      run_pass(h, *g, P, st, M_MERGE);
       commit(h, *g, st);
     }
     LV_CUDA(cudaStreamSynchronize(c.s));
@@ -406,7 +529,7 @@ void run_impl(louvain_ctx *h) {
     double t3 = now_ms();
     st = State();
     auto hg = std::make_unique<DGraph>();
-    contract(c, *g, B, rec->labels.p, k, std::move(ndelta), *hg);
+    contract(c, *g, P.all(c, *g), rec->labels.p, k, std::move(ndelta), *hg);
     double t4 = now_ms();
     rec->q = q_of_contracted(h, *hg);
     rec->times[1] = t1 - t0;
@@ -498,11 +621,27 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       LV_CUDA(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
       h->own_stream = true;
     }
+    if (!getenv("LV_SERIAL")) h->c.init_side();  // concurrent degree bins (LV_SERIAL=1: off)
     h->c.A.a = cfg.alloc;
     h->c.A.f = cfg.free;
     h->c.A.ctx = cfg.alloc_ctx;
     h->c.A.s = h->c.s;
-    LV_CUDA(cudaMallocHost((void **)&h->hctr, NBIN * 8 * sizeof(u64)));
+    if (cfg.nccl_comm) {
+      LV_REQUIRE(cfg.world >= 1 && cfg.rank >= 0 && cfg.rank < cfg.world, LV_EINVAL, "bad rank/world");
+      h->shard = true;
+      h->comm = cfg.nccl_comm;
+      h->world = cfg.world;
+      h->rank = cfg.rank;
+    } else if (const char *e = getenv("LV_SHARD_SIM")) {  // tests: P virtual ranks in-process
+      const int P = atoi(e);
+      if (P >= 1) {
+        h->shard = true;
+        h->sim = P;
+        h->world = P;
+      }
+    }
+    const size_t nslots = (size_t)(h->world + 1) * NBIN * 8;
+    LV_CUDA(cudaMallocHost((void **)&h->hctr, nslots * sizeof(u64)));
     if (const char *e = getenv("LV_L2MODE")) h->l2mode = atoi(e);
     if (h->l2mode & 4) {
       int maxp = 0, maxw = 0;
@@ -511,7 +650,7 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       LV_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
       h->l2win = std::min<size_t>((size_t)maxp, (size_t)maxw);
     }
-    h->dctr.alloc(h->c.A, NBIN * 8);
+    h->dctr.alloc(h->c.A, nslots);
     // input to device
     const int32_t *src = gr->src, *dst = gr->dst;
     const void *w = gr->w;
@@ -640,10 +779,11 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     LV_CUDA(cudaStreamSynchronize(c.s));
     LV_REQUIRE(herr == 0, LV_EINVAL, "labels must lie in [0,n)");
     // the sweep pass also yields Σ e_{i->C(i)} of the snapshot; merge mode reuses it
-    SweepOut o = run_pass(h, g, B, st, M_SWEEP);
+    const Plan P = plan_of(B);
+    SweepOut o = run_pass(h, g, P, st, M_SWEEP);
     if (mode == 1) {
       const u64 i2_snap = o.i2;
-      o = run_pass(h, g, B, st, M_MERGE);
+      o = run_pass(h, g, P, st, M_MERGE);
       o.i2 = i2_snap;
     }
     // exact Eq. 3 numerators of the snapshot (S2 over all labels, not the fused form)
@@ -678,8 +818,9 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
     Bins &B = vbins0(h);
     State st;
     init_state(h, g, st);
+    const Plan PL = plan_of(B);
     for (int i = 0; i < warm; ++i) {
-      run_pass(h, g, B, st, M_SWEEP);
+      run_pass(h, g, PL, st, M_SWEEP);
       commit(h, g, st);
     }
     LV_CUDA(cudaStreamSynchronize(c.s));
@@ -693,7 +834,7 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
     for (int r = 0; r < reps; ++r) {
       std::vector<SweepOut> pb;
       LV_CUDA(cudaEventRecord(e0, c.s));
-      SweepOut o = run_pass(h, g, B, st, M_SWEEP, &tm, &pb);  // includes the counter D2H sync
+      SweepOut o = run_pass(h, g, PL, st, M_SWEEP, &tm, &pb);  // includes the counter D2H sync
       commit(h, g, st, &tm);
       LV_CUDA(cudaEventRecord(e1, c.s));
       LV_CUDA(cudaEventSynchronize(e1));
@@ -837,6 +978,24 @@ louvain_status louvain_nccl_init(const uint8_t id[128], int32_t world, int32_t r
   nccl_uid_t u;
   memcpy(u.internal, id, 128);
   return f(comm_out, world, u, rank) == 0 ? LV_OK : LV_ENCCL;
+}
+
+louvain_status louvain_shard_bounds(const int64_t *row_ptr, int64_t n, int32_t world, int64_t *bounds) {
+  if (!row_ptr || !bounds || n < 0 || world < 1) return LV_EINVAL;
+  const i64 nnz = row_ptr[n];
+  bounds[0] = 0;
+  bounds[world] = n;
+  for (int p = 1; p < world; ++p) {
+    const i64 target = (i64)(((__int128)nnz * p) / world);
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (row_ptr[mid] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    bounds[p] = lo;
+  }
+  return LV_OK;
 }
 
 louvain_status louvain_nccl_destroy(void *comm) {

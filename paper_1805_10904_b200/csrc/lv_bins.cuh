@@ -30,29 +30,37 @@ __device__ __forceinline__ int bin_of(i64 d) {
   return 8;
 }
 
-struct KTimer {  // optional per-launch CUDA-event timing (louvain_time_sweeps)
+struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
   bool on = false;
   std::vector<std::string> names;
-  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<cudaEvent_t> t0, t1;
+  std::vector<size_t> open;
   void begin(cudaStream_t s, const std::string &n) {
     if (!on) return;
     cudaEvent_t a;
     cudaEventCreate(&a);
     cudaEventRecord(a, s);
     names.push_back(n);
-    ev.push_back(a);
+    t0.push_back(a);
+    t1.push_back(nullptr);
+    open.push_back(names.size() - 1);
   }
   void end(cudaStream_t s) {
-    if (!on) return;
+    if (!on || open.empty()) return;
     cudaEvent_t b;
     cudaEventCreate(&b);
     cudaEventRecord(b, s);
-    ev.push_back(b);
+    t1[open.back()] = b;
+    open.pop_back();
   }
   void clear() {
-    for (auto e : ev) cudaEventDestroy(e);
-    ev.clear();
+    for (auto e : t0) cudaEventDestroy(e);
+    for (auto e : t1)
+      if (e) cudaEventDestroy(e);
+    t0.clear();
+    t1.clear();
     names.clear();
+    open.clear();
   }
   ~KTimer() { clear(); }
 };
@@ -81,9 +89,27 @@ struct LenOf {
   __device__ __forceinline__ i64 operator()(i64 r) const { return ptr[r + 1] - ptr[r]; }
 };
 
-__global__ void k_bin_ids(i64 n, const i64 *__restrict__ ptr, uint8_t *ids) {
+__global__ void k_bin_ids(i64 n, const i64 *__restrict__ ptr, uint8_t *ids, i64 lo, i64 hi) {
   for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256)
-    ids[r] = (uint8_t)bin_of(ptr[r + 1] - ptr[r]);
+    ids[r] = (r >= lo && r < hi) ? (uint8_t)bin_of(ptr[r + 1] - ptr[r]) : (uint8_t)255;
+}
+
+// Edge-balanced contiguous vertex ranges (sweep-sharded mode):
+// bounds[p] = first row v with ptr[v] >= p·nnz/P (bounds[0] = 0, bounds[P] = n).
+__global__ void k_shard_bounds(i64 n, const i64 *__restrict__ ptr, int P, i64 *bounds) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > P) return;
+  if (p == 0) { bounds[0] = 0; return; }
+  if (p == P) { bounds[P] = n; return; }
+  const i64 nnz = ptr[n];
+  const i64 target = (i64)(((__int128)nnz * p) / P);
+  i64 lo = 0, hi = n;  // first v in [0,n] with ptr[v] >= target
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (ptr[mid] >= target) hi = mid;
+    else lo = mid + 1;
+  }
+  bounds[p] = lo;
 }
 
 struct BinLen {
@@ -122,11 +148,13 @@ inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
 
 // Partition rows [0,nrows) of `ptr` into length bins; set up hub tables sized for at
 // most `universe` distinct keys per row.
-inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B) {
+// Only rows in [lo, hi) are binned (hi < 0: all rows).
+inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B, i64 lo = 0, i64 hi = -1) {
   B.nrows = nrows;
+  if (hi < 0) hi = nrows;
   Buf<uint8_t> ids(c.A, nrows > 0 ? nrows : 1);
   Buf<i64> pos(c.A, nrows + 1);
-  LV_LAUNCH(c, k_bin_ids, grid_for(c, nrows), 256, 0, nrows, ptr, ids.p);
+  LV_LAUNCH(c, k_bin_ids, grid_for(c, nrows), 256, 0, nrows, ptr, ids.p, lo, hi);
   // counts per bin
   std::vector<i64> cnt(NBIN, 0);
   for (int b = 0; b < NBIN; ++b) {
@@ -223,7 +251,7 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B)
 
 // ----------------------------------------------------------------- launch
 template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
-void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
+void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st) {
   auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT, VT>;
   constexpr int GPB = BLOCK / G;
   const size_t smem = smem_bytes<G, CAP, BLOCK, VT>();
@@ -237,9 +265,9 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag) {
   i64 grid = cdiv(a.nrows, GPB);
   i64 cap = (i64)c.sms * occ * 8;
   if (grid > cap) grid = cap;
-  if (tm) tm->begin(c.s, tag);
-  LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, smem, a);
-  if (tm) tm->end(c.s);
+  if (tm) tm->begin(st, tag);  // events on the launching stream
+  LV_LAUNCH_ON(c, st, kern, (unsigned)grid, BLOCK, smem, a);
+  if (tm) tm->end(st);
 }
 
 static const char *BIN_NAME[NBIN] = {"agg_g4_c8",      "agg_g8_c16",      "agg_g16_c32",
@@ -258,6 +286,12 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     a.counters = ctr ? ctr + 8 * b : nullptr;
   };
   std::string pre = std::string(MN[MODE]) + ":";
+  const bool conc = c.concurrent;
+  if (conc) {  // fork: side streams start after everything already queued on the handle stream
+    LV_CUDA(cudaEventRecord(c.fork_ev, c.s));
+    for (int i = 0; i < Ctx::NSIDE; ++i) LV_CUDA(cudaStreamWaitEvent(c.side[i], c.fork_ev, 0));
+  }
+  cudaStream_t hub_s = conc ? c.side[0] : c.s;
   // hub path first (longest rows), then the big bins, then the small ones
   if (B.nhub) {
     set(NSMEM);
@@ -288,15 +322,31 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
                                    (int)hub_fin_smem<VT>()));
       attr_fin = true;
     }
-    if (tm) tm->begin(c.s, pre + "hub_acc");
-    LV_LAUNCH(c, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, acc_smem, a, hb);
-    if (tm) tm->end(c.s);
-    if (tm) tm->begin(c.s, pre + "hub_fin");
-    LV_LAUNCH(c, (k_hub_fin<MODE, VT>), (unsigned)B.nfin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
-    if (tm) tm->end(c.s);
-    if (tm) tm->begin(c.s, pre + "hub_decide");
-    LV_LAUNCH(c, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
-    if (tm) tm->end(c.s);
+    if (tm) tm->begin(hub_s, pre + "hub_acc");
+    LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, acc_smem, a, hb);
+    if (tm) tm->end(hub_s);
+    if (tm) tm->begin(hub_s, pre + "hub_fin");
+    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)B.nfin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
+    if (tm) tm->end(hub_s);
+    if (tm) tm->begin(hub_s, pre + "hub_decide");
+    LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
+    if (tm) tm->end(hub_s);
+  }
+  // bins in decreasing length; concurrent mode spreads them over the side streams
+  auto st = [&](int k) { return conc ? c.side[(k + 1) % Ctx::NSIDE] : c.s; };
+  if (B.count(7)) { set(7); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[7]).c_str(), st(0)); }
+  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str(), st(1)); }
+  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str(), st(2)); }
+  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[4]).c_str(), st(0)); }
+  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str(), st(1)); }
+  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str(), st(2)); }
+  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str(), st(0)); }
+  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[0]).c_str(), st(1)); }
+  if (conc) {  // join: the handle stream waits for every side stream
+    for (int i = 0; i < Ctx::NSIDE; ++i) {
+      LV_CUDA(cudaEventRecord(c.join_ev[i], c.side[i]));
+      LV_CUDA(cudaStreamWaitEvent(c.s, c.join_ev[i], 0));
+    }
   }
   if (B.nhub) {  // a bucket beyond HUB_FIN_MAXD distinct keys would have been dropped
     int ovf = 0;
@@ -304,14 +354,6 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     LV_CUDA(cudaStreamSynchronize(c.s));
     LV_REQUIRE(ovf == 0, LV_ECUDA, "hub bucket overflow (a hash bucket exceeded its table)");
   }
-  if (B.count(7)) { set(7); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[7]).c_str()); }
-  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str()); }
-  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str()); }
-  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[4]).c_str()); }
-  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str()); }
-  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str()); }
-  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str()); }
-  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[0]).c_str()); }
 }
 
 template <int MODE>

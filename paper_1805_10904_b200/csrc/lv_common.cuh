@@ -109,14 +109,42 @@ struct Buf {
 struct Ctx {
   int device = 0;
   int sms = 148;
-  cudaStream_t s = nullptr;
+  cudaStream_t s = nullptr;  // the handle's stream: every public call is ordered on it
   Alloc A;
   i64 launches = 0;
+  // fork/join pool for independent kernels of one pass (degree bins run concurrently)
+  static constexpr int NSIDE = 4;
+  cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
+  bool concurrent = false;
+  void init_side() {
+    for (int i = 0; i < NSIDE; ++i) {
+      if (cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking) != cudaSuccess) return;
+      cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+    concurrent = true;
+  }
+  void free_side() {
+    for (int i = 0; i < NSIDE; ++i) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (join_ev[i]) cudaEventDestroy(join_ev[i]);
+    }
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    concurrent = false;
+  }
 };
 
 #define LV_LAUNCH(ctx, kern, grid, block, smem, ...)                          \
   do {                                                                        \
     kern<<<(grid), (block), (smem), (ctx).s>>>(__VA_ARGS__);                  \
+    (ctx).launches++;                                                         \
+    LV_CUDA(cudaGetLastError());                                              \
+  } while (0)
+
+#define LV_LAUNCH_ON(ctx, strm, kern, grid, block, smem, ...)                 \
+  do {                                                                        \
+    kern<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);                   \
     (ctx).launches++;                                                         \
     LV_CUDA(cudaGetLastError());                                              \
   } while (0)
