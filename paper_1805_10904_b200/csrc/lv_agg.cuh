@@ -55,8 +55,16 @@ struct Chunk {
   int32_t h, pad;
 };
 
+// Packed per-row header of a bin (built once per level): one 16-byte load per row
+// instead of rows[] -> row_ptr[] -> row_ptr[+1].
+struct RowHdr {
+  i64 beg;
+  int32_t r, len;
+};
+
 struct AggArgs {
   const i64 *ptr;          // row offsets: row r = [ptr[r], ptr[r+1])
+  const RowHdr *hdr;       // headers of this bin's rows (smem bins)
   const int32_t *rows;     // rows of this bin
   i64 nrows;
   const int32_t *keys;     // SWEEP/MERGE: col[] (key = label[col]); EMIT: key directly
@@ -143,7 +151,10 @@ template <int G, int U, int MODE, class WT, bool SHARED, bool LIST, class VT>
 __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, VT *vals,
                                              unsigned mask, int lg, uint16_t *olist, int *ocnt) {
   const u64 pf = l2_policy_first(), pl = l2_policy_last();
-  for (i64 e0 = beg + lane; e0 < end; e0 += (i64)G * U) {
+  // lane-uniform trip count (every lane of the group runs every batch): required by the
+  // warp-synchronous pre-aggregation below
+  for (i64 b0 = beg; b0 < end; b0 += (i64)G * U) {
+    const i64 e0 = b0 + lane;
     int32_t k[U];
     u64 wv[U];
 #pragma unroll
@@ -168,9 +179,10 @@ __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      const u64 wsum = wv[u];
       if (k[u] < 0) continue;
       bool claimed = false;
-      const unsigned sl = tab_insert<SHARED, VT>(keys, vals, mask, lg, k[u], wv[u], LIST ? &claimed : nullptr);
+      const unsigned sl = tab_insert<SHARED, VT>(keys, vals, mask, lg, k[u], wsum, LIST ? &claimed : nullptr);
       if (LIST && claimed) olist[atomicAdd(ocnt, 1)] = (uint16_t)sl;
     }
   }
@@ -198,6 +210,7 @@ struct Cand {  // lexicographic key (S desc, c asc); c == INT32_MAX means "none"
   i64 hi;
   u64 lo;
   int32_t c;
+  int32_t sg;  // |C| == 1 (singlet rule), carried with the candidate
 };
 
 __device__ __forceinline__ i128 cand_S(const Cand &x) { return (i128)(((u128)(u64)x.hi << 64) | (u128)x.lo); }
@@ -335,7 +348,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
   constexpr int U = G < 32 ? 2 : 4;  // entries per lane per batch: their deg_C gathers overlap
   if (MODE == M_SWEEP) {
     Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
     u64 eown = 0, ncand = 0;
     int32_t dummy = 0;
     for (i64 t0 = g.lane; t0 < n; t0 += (i64)G * U) {
@@ -358,7 +371,9 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (k[u] < 0) continue;
@@ -379,7 +394,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
       int32_t tgt = own;
       if (best.c != INT32_MAX && cand_S(best) > S_own) {
         tgt = best.c;
-        if (pre.szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule
+        if (pre.szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule (D8)
       }
       a.label_next[r] = tgt;
       if (tgt != own) record_move(a, own, tgt, di);
@@ -390,7 +405,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
     }
   } else if (MODE == M_MERGE) {
     Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
     u64 cnt = 0, unused = 0;
     int32_t T = -1;
     for (i64 t = g.lane; t < n; t += G) {
@@ -440,7 +455,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
       }
     }
     Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
     int32_t dummy = 0;
     grp_reduce<G, BLOCK>(g, none, selfw, sumw, dummy);
     if (g.lane == 0) {
@@ -486,9 +501,16 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   for (int s = g.lane; s < CAP; s += G) { keys[s] = -1; vals[s] = 0; }
   if (LIST && g.lane == 0) *ocnt = 0;
   g.sync();
-  for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < a.nrows; idx += (i64)gridDim.x * GPB) {
-    const int32_t r = a.rows[idx];
-    const i64 beg = a.ptr[r], end = a.ptr[r + 1];
+  const i64 stride = (i64)gridDim.x * GPB;
+  i64 idx = (i64)blockIdx.x * GPB + grp;
+  RowHdr nh;  // next row's header, prefetched one iteration ahead
+  nh.beg = 0; nh.r = 0; nh.len = 0;
+  if (idx < a.nrows) nh = a.hdr[idx];
+  for (; idx < a.nrows; idx += stride) {
+    const RowHdr hd = nh;
+    if (idx + stride < a.nrows) nh = a.hdr[idx + stride];
+    const int32_t r = hd.r;
+    const i64 beg = hd.beg, end = hd.beg + hd.len;
     const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
     const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
     RowPre pre;
@@ -513,6 +535,146 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     g.sync();
     if (LIST && g.lane == 0) *ocnt = 0;
     g.sync();
+  }
+  if (MODE != M_EMIT) acc.flush(a.counters);
+}
+
+// ----------------------------------------------------------------- register bins
+// Rows of length <= G <= 32: one edge per lane, no shared memory.  Lanes holding the same
+// key are found with __match_any_sync and their weights summed (__reduce_add_sync when the
+// row sum fits 32 bits, else an exact shuffle loop); the first lane of each key group
+// stands for that candidate community.
+template <int G, int BLOCK, int MODE, class WT, bool NARROW>
+__global__ void __launch_bounds__(BLOCK) k_agg_reg(AggArgs a) {
+  constexpr int GPB = BLOCK / G;
+  Grp<G, BLOCK> g;
+  const int grp = threadIdx.x / G;
+  const int wl = threadIdx.x & 31;
+  Acc acc;
+  const u64 pf = l2_policy_first();
+  const i64 stride = (i64)gridDim.x * GPB;
+  i64 idx = (i64)blockIdx.x * GPB + grp;
+  RowHdr nh;
+  nh.beg = 0; nh.r = 0; nh.len = 0;
+  if (idx < a.nrows) nh = a.hdr[idx];
+  for (; idx < a.nrows; idx += stride) {
+    const RowHdr hd = nh;
+    if (idx + stride < a.nrows) nh = a.hdr[idx + stride];
+    const int32_t r = hd.r;
+    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    i64 di = 0, dq = 0, dr = 0;
+    int32_t szo = 0;
+    if (MODE == M_SWEEP) {
+      di = a.delta[r];
+      if (g.lane == 0) {
+        dq = __ldg(&a.deg[own]);
+        dr = __ldg(&a.deg[r]);
+        szo = __ldg(&a.size[own]);
+      }
+    }
+    if (MODE == M_MERGE) {
+      if (a.size[own] != 1) {
+        if (g.lane == 0) a.label_next[r] = own;
+        continue;
+      }
+    }
+    int32_t k = -1;
+    u64 w = 0;
+    if (g.lane < hd.len) {
+      const i64 e = hd.beg + g.lane;
+      if (a.hint & 1) {
+        k = ld_stream(&a.keys[e], pf);
+        w = WT::get(a.w, e, pf);
+      } else {
+        k = __ldg(&a.keys[e]);
+        w = WT::get(a.w, e);
+      }
+      if (MODE != M_EMIT) k = __ldg(&a.label[k]);
+    }
+    bool lead;
+    u64 sum;
+    if (G <= 8 || !NARROW) {  // small groups: an O(G) shuffle scan beats MATCH.ANY
+      constexpr int W = G < 32 ? G : 32;
+      sum = 0;
+      bool first = true;
+      const int gl = g.lane;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const int32_t kj = __shfl_sync(g.mask, k, j, W);
+        const u64 wj = NARROW ? (u64)__shfl_sync(g.mask, (uint32_t)w, j, W) : __shfl_sync(g.mask, w, j, W);
+        if (kj == k) {
+          sum += wj;
+          if (j < gl) first = false;
+        }
+      }
+      lead = first && k >= 0;
+    } else {
+      const unsigned peers = __match_any_sync(g.mask, k);
+      lead = (__ffs(peers) - 1) == wl && k >= 0;
+      sum = __reduce_add_sync(peers, (uint32_t)w);
+    }
+    if (MODE == M_SWEEP) {
+      Cand best;
+      best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
+      u64 eown = 0, ncand = 0;
+      int32_t dummy = 0;
+      if (lead) {
+        if (k == own) {
+          eown = sum;
+        } else {
+          ncand = 1;
+          const i64 dk = (a.hint & 2) ? ld_keep(&a.deg[k], l2_policy_last()) : __ldg(&a.deg[k]);
+          const i128 S = move_score(a.twoW, sum, di, dk);
+          best.hi = (i64)(S >> 64); best.lo = (u64)S; best.c = k;
+        }
+      }
+      grp_reduce<G, BLOCK>(g, best, eown, ncand, dummy);
+      if (g.lane == 0) {
+        const i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
+        int32_t tgt = own;
+        if (best.c != INT32_MAX && cand_S(best) > S_own) {
+          tgt = best.c;
+          if (szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule (D8)
+        }
+        a.label_next[r] = tgt;
+        if (tgt != own) record_move(a, own, tgt, di);
+        acc.moved += (tgt != own);
+        acc.i2 += eown;
+        acc.cand += ncand;
+        acc.add_sq(dr);
+      }
+    } else if (MODE == M_MERGE) {
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
+      u64 cnt = (lead && k != own) ? 1 : 0, unused = 0;
+      int32_t T = (lead && k != own) ? k : -1;
+      grp_reduce<G, BLOCK>(g, none, cnt, unused, T);
+      if (g.lane == 0) {
+        int32_t tgt = own;
+        if (cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
+        a.label_next[r] = tgt;
+        if (tgt != own) record_move(a, own, tgt, a.delta[r]);
+        acc.moved += (tgt != own);
+      }
+    } else {  // M_EMIT: distinct keys != r written compactly at out_base[r]
+      const bool emit = lead && k != r;
+      const unsigned bal = __ballot_sync(g.mask, emit) & g.mask;
+      if (emit && a.out_key) {
+        const i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + __popc(bal & ((1u << wl) - 1u));
+        a.out_key[o] = k;
+        a.out_w[o] = sum;
+      }
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
+      u64 selfw = (lead && k == r) ? sum : 0, sumw = lead ? sum : 0;
+      int32_t dummy = 0;
+      grp_reduce<G, BLOCK>(g, none, selfw, sumw, dummy);
+      if (g.lane == 0) {
+        a.out_cnt[r] = (i64)__popc(bal);
+        if (a.out_self) a.out_self[r] = selfw;
+        if (a.out_sum) a.out_sum[r] = sumw;
+      }
+    }
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
@@ -546,7 +708,7 @@ __device__ __forceinline__ unsigned hbucket(int32_t k, int blg) {
 struct HubPartial {
   i64 hi;
   u64 lo;
-  int32_t c, T;
+  int32_t c, T, sg, pad;
   u64 eown, cnt, selfw, sumw;
 };
 
@@ -668,7 +830,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   const int32_t r = a.rows[h];
   const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
   HubPartial P;
-  P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1;
+  P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1; P.sg = 0; P.pad = 0;
   P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
   if (MODE == M_MERGE && a.size[own] != 1) {
     if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
@@ -721,7 +883,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     const i64 di = a.delta[r];
     constexpr int U = 4;
     Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
     u64 eown = 0, n1 = 0;
     int32_t dm = 0;
     for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
@@ -740,7 +902,9 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (k[u] < 0) continue;
@@ -756,10 +920,10 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
       }
     }
     grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
-    if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
+    if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.sg = best.sg; P.eown = eown; P.cnt = n1; }
   } else if (MODE == M_MERGE) {
     Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
     u64 n1 = 0, unused = 0;
     int32_t T = -1;
     for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
@@ -794,7 +958,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
       }
     }
     Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX;
+    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
     int32_t dm = 0;
     grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
     if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
@@ -810,14 +974,14 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     const int32_t r = a.rows[h];
     const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
     Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX;
+    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
     u64 eown = 0, cnt = 0, selfw = 0, sumw = 0;
     int32_t T = -1;
     const HubPartial *p = hb.part + hb.bfirst[h];
     const int np = 1 << hb.blg[h];
     for (int j = 0; j < np; ++j) {
       Cand x;
-      x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
+      x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c; x.sg = p[j].sg;
       if (cand_better(x, best)) best = x;
       eown += p[j].eown; cnt += p[j].cnt; selfw += p[j].selfw; sumw += p[j].sumw;
       T = max(T, p[j].T);

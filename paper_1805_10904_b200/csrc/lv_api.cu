@@ -621,7 +621,7 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       LV_CUDA(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
       h->own_stream = true;
     }
-    if (!getenv("LV_SERIAL")) h->c.init_side();  // concurrent degree bins (LV_SERIAL=1: off)
+    if (getenv("LV_CONCURRENT")) h->c.init_side();  // degree bins on side streams (measured slower)
     h->c.A.a = cfg.alloc;
     h->c.A.f = cfg.free;
     h->c.A.ctx = cfg.alloc_ctx;

@@ -68,6 +68,7 @@ struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
 struct Bins {
   i64 nrows = 0;             // universe of rows considered
   Buf<int32_t> rows;         // active rows grouped by bin (ascending id within a bin)
+  Buf<RowHdr> hdr;           // packed {beg, r, len} per entry of rows
   i64 off[NBIN + 1] = {0};   // host offsets of each bin in rows
   i64 edges[NBIN] = {0};     // Σ row length per bin
   // hub path (see lv_agg.cuh): chunks, buckets, pool, segment tables, partials
@@ -130,6 +131,17 @@ __global__ void k_bin_scatter(i64 n, const uint8_t *__restrict__ ids, int b, con
     if (ids[r] == b) out[pos[r]] = (int32_t)r;
 }
 
+__global__ void k_fill_hdr(i64 m, const int32_t *__restrict__ rows, const i64 *__restrict__ ptr, RowHdr *hdr) {
+  for (i64 t = (i64)blockIdx.x * 256 + threadIdx.x; t < m; t += (i64)gridDim.x * 256) {
+    const int32_t r = rows[t];
+    RowHdr h;
+    h.beg = ptr[r];
+    h.r = r;
+    h.len = (int32_t)(ptr[r + 1] - ptr[r]);
+    hdr[t] = h;
+  }
+}
+
 __global__ void k_gather_len(i64 m, const int32_t *rows, const i64 *ptr, i64 *beg, i64 *len) {
   for (i64 t = (i64)blockIdx.x * 256 + threadIdx.x; t < m; t += (i64)gridDim.x * 256) {
     int32_t r = rows[t];
@@ -169,6 +181,9 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     exclusive_scan<i64>(c, IsBin{ids.p, b}, nrows, pos.p, false);
     LV_LAUNCH(c, k_bin_scatter, grid_for(c, nrows), 256, 0, nrows, ids.p, b, pos.p, B.rows.p + B.off[b]);
   }
+  B.hdr.alloc(c.A, B.off[NBIN] > 0 ? B.off[NBIN] : 1);
+  if (B.off[NSMEM] > 0)
+    LV_LAUNCH(c, k_fill_hdr, grid_for(c, B.off[NSMEM]), 256, 0, B.off[NSMEM], B.rows.p, ptr, B.hdr.p);
   {
     Buf<u64> es(c.A, NBIN);
     LV_CUDA(cudaMemsetAsync(es.p, 0, NBIN * sizeof(u64), c.s));
@@ -250,6 +265,25 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
 }
 
 // ----------------------------------------------------------------- launch
+template <int G, int BLOCK, int MODE, class WT, class VT>
+void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st) {
+  constexpr bool NARROW = sizeof(VT) == 4;
+  auto kern = k_agg_reg<G, BLOCK, MODE, WT, NARROW>;
+  constexpr int GPB = BLOCK / G;
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, 0));
+    occ = o > 0 ? o : 1;
+  }
+  i64 grid = cdiv(a.nrows, GPB);
+  i64 cap = (i64)c.sms * occ * 8;
+  if (grid > cap) grid = cap;
+  if (tm) tm->begin(st, tag);
+  LV_LAUNCH_ON(c, st, kern, (unsigned)grid, BLOCK, 0, a);
+  if (tm) tm->end(st);
+}
+
 template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st) {
   auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT, VT>;
@@ -270,8 +304,8 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   if (tm) tm->end(st);
 }
 
-static const char *BIN_NAME[NBIN] = {"agg_g4_c8",      "agg_g8_c16",      "agg_g16_c32",
-                                     "agg_g32_c64",    "agg_g32_c256",    "agg_blk128_c1024",
+static const char *BIN_NAME[NBIN] = {"reg_g4",         "reg_g8",          "reg_g16",
+                                     "reg_g32",        "agg_g32_c256",    "agg_blk128_c1024",
                                      "agg_blk256_c4096", "agg_blk512_c8192", "agg_hub"};
 
 // One pass of MODE over every bin of B.  `a` carries the common arguments.  VT is the
@@ -282,6 +316,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   u64 *ctr = a.counters;  // NBIN slots of 8 counters (one per bin) or NULL
   auto set = [&](int b) {
     a.rows = B.rows.p + B.off[b];
+    a.hdr = B.hdr.p + B.off[b];
     a.nrows = B.count(b);
     a.counters = ctr ? ctr + 8 * b : nullptr;
   };
@@ -338,10 +373,10 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str(), st(1)); }
   if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str(), st(2)); }
   if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[4]).c_str(), st(0)); }
-  if (B.count(3)) { set(3); launch_bin<32, 64, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str(), st(1)); }
-  if (B.count(2)) { set(2); launch_bin<16, 32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str(), st(2)); }
-  if (B.count(1)) { set(1); launch_bin<8, 16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str(), st(0)); }
-  if (B.count(0)) { set(0); launch_bin<4, 8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[0]).c_str(), st(1)); }
+  if (B.count(3)) { set(3); launch_reg<32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str(), st(1)); }
+  if (B.count(2)) { set(2); launch_reg<16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str(), st(2)); }
+  if (B.count(1)) { set(1); launch_reg<8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str(), st(0)); }
+  if (B.count(0)) { set(0); launch_reg<4, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[0]).c_str(), st(1)); }
   if (conc) {  // join: the handle stream waits for every side stream
     for (int i = 0; i < Ctx::NSIDE; ++i) {
       LV_CUDA(cudaEventRecord(c.join_ev[i], c.side[i]));
