@@ -725,7 +725,7 @@ struct HubArgs {
   HubPartial *part;       // per fin item
   u64 *emit_cur;          // per hub (EMIT output cursor)
   int *overflow;          // set if a bucket exceeds HUB_FIN_MAXD distinct keys
-  i64 nhub;
+  i64 nhub, nchunks, nfin;
 };
 
 template <class VT>
@@ -774,6 +774,8 @@ __device__ __forceinline__ int smem_excl_scan(int *cnt, int n) {
   return total;
 }
 
+// Persistent: each CTA loops over chunks; the shared table is cleared once and every
+// used slot is reset through the occupied list.
 template <int MODE, class WT, class VT>
 __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -783,38 +785,46 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   uint16_t *slist = (uint16_t *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)));
   int *hist = (int *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t));
   __shared__ int scnt;
-  const Chunk ch = a.chunks[blockIdx.x];
-  const int32_t r = a.rows[ch.h];
-  if (MODE == M_MERGE) {
-    if (a.size[a.label[r]] != 1) return;
-  }
   for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
-  const int blg = hb.blg[ch.h];
-  const int nb = 1 << blg;
-  for (int b = threadIdx.x; b <= nb; b += HUB_ACC_T) hist[b] = 0;
   if (threadIdx.x == 0) scnt = 0;
   __syncthreads();
-  insert_range<HUB_ACC_T, 8, MODE, WT, true, true, VT>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1,
-                                                       HUB_SM_LG, slist, &scnt);
-  __syncthreads();
-  const int n = scnt;
-  for (int t = threadIdx.x; t < n; t += HUB_ACC_T) atomicAdd(&hist[hbucket(skeys[slist[t]], blg)], 1);
-  __syncthreads();
-  smem_excl_scan<HUB_ACC_T>(hist, nb);  // hist[b] = start of bucket b
-  int32_t *seg = hb.seg + hb.segoff[blockIdx.x];
-  for (int b = threadIdx.x; b < nb; b += HUB_ACC_T) seg[b] = hist[b];
-  if (threadIdx.x == 0) seg[nb] = n;
-  __syncthreads();
-  const i64 base = (i64)blockIdx.x * HUB_CHUNK;
-  for (int t = threadIdx.x; t < n; t += HUB_ACC_T) {
-    const int sl = slist[t];
-    const int32_t k = skeys[sl];
-    const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
-    hb.pkey[base + pos] = k;
-    hb.pval[base + pos] = (u64)svals[sl];
+  for (i64 ci = blockIdx.x; ci < hb.nchunks; ci += gridDim.x) {
+    const Chunk ch = a.chunks[ci];
+    const int32_t r = a.rows[ch.h];
+    if (MODE == M_MERGE) {
+      if (a.size[a.label[r]] != 1) continue;  // CTA-uniform
+    }
+    const int blg = hb.blg[ch.h];
+    const int nb = 1 << blg;
+    for (int b = threadIdx.x; b <= nb; b += HUB_ACC_T) hist[b] = 0;
+    insert_range<HUB_ACC_T, 8, MODE, WT, true, true, VT>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1,
+                                                         HUB_SM_LG, slist, &scnt);
+    __syncthreads();
+    const int n = scnt;
+    for (int t = threadIdx.x; t < n; t += HUB_ACC_T) atomicAdd(&hist[hbucket(skeys[slist[t]], blg)], 1);
+    __syncthreads();
+    smem_excl_scan<HUB_ACC_T>(hist, nb);  // hist[b] = start of bucket b
+    int32_t *seg = hb.seg + hb.segoff[ci];
+    for (int b = threadIdx.x; b < nb; b += HUB_ACC_T) seg[b] = hist[b];
+    if (threadIdx.x == 0) seg[nb] = n;
+    __syncthreads();
+    const i64 base = ci * HUB_CHUNK;
+    for (int t = threadIdx.x; t < n; t += HUB_ACC_T) {
+      const int sl = slist[t];
+      const int32_t k = skeys[sl];
+      const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
+      hb.pkey[base + pos] = k;
+      hb.pval[base + pos] = (u64)svals[sl];
+      skeys[sl] = -1;
+      svals[sl] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) scnt = 0;
+    __syncthreads();
   }
 }
 
+// Persistent over (row, bucket) items; table reset through the occupied list.
 template <int MODE, class VT>
 __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -825,145 +835,150 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   i64 *tst = (i64 *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_FIN_MAXD * sizeof(uint16_t));
   int *tlen = (int *)(tst + HUB_FIN_TILE);
   __shared__ int scnt, sovf;
-  const int2 it = hb.fitem[blockIdx.x];
-  const int h = it.x, b = it.y;
-  const int32_t r = a.rows[h];
-  const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
-  HubPartial P;
-  P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1; P.sg = 0; P.pad = 0;
-  P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
-  if (MODE == M_MERGE && a.size[own] != 1) {
-    if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
-    return;
-  }
+  __shared__ u64 sbase;
   for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = -1; svals[s] = 0; }
   if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
   __syncthreads();
-  const int blg = hb.blg[h];
-  const i64 cf = hb.cfirst[h];
-  const int nch = hb.ccount[h];
-  for (int t0 = 0; t0 < nch; t0 += HUB_FIN_TILE) {
-    const int m = min(HUB_FIN_TILE, nch - t0);
-    for (int j = threadIdx.x; j < m; j += HUB_FIN_T) {
-      const i64 c = cf + t0 + j;
-      const int32_t *seg = hb.seg + hb.segoff[c];
-      const int s0 = seg[b], s1 = seg[b + 1];
-      tlen[j] = s1 - s0;
-      tst[j] = c * HUB_CHUNK + s0;
-    }
-    __syncthreads();
-    const int total = smem_excl_scan<HUB_FIN_T>(tlen, m);  // tlen[j] = prefix
-    for (int t = threadIdx.x; t < total; t += HUB_FIN_T) {
-      int lo = 0, hi = m - 1;  // last j with tlen[j] <= t
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (tlen[mid] <= t) lo = mid;
-        else hi = mid - 1;
-      }
-      const i64 e = tst[lo] + (t - tlen[lo]);
-      const int32_t k = hb.pkey[e];
-      const u64 v = hb.pval[e];
-      if (*(volatile int *)&scnt >= HUB_FIN_MAXD - 1) { sovf = 1; continue; }
-      bool claimed = false;
-      const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, HUB_FIN_LG, k, v, &claimed);
-      if (claimed) {
-        const int q = atomicAdd(&scnt, 1);
-        if (q < HUB_FIN_MAXD) slist[q] = (uint16_t)sl;
-        else sovf = 1;
-      }
-    }
-    __syncthreads();
-  }
-  if (sovf) {
-    if (threadIdx.x == 0) atomicOr(hb.overflow, 1);
-  }
-  const int n = min(scnt, HUB_FIN_MAXD);
   Grp<HUB_FIN_T, HUB_FIN_T> g;
-  if (MODE == M_SWEEP) {
-    const i64 di = a.delta[r];
-    constexpr int U = 4;
-    Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
-    u64 eown = 0, n1 = 0;
-    int32_t dm = 0;
-    for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
-      int32_t k[U];
-      u64 v[U];
-      i64 dk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u * HUB_FIN_T;
-        k[u] = -1;
-        v[u] = 0;
-        if (t < n) {
-          const int sl = slist[t];
-          k[u] = skeys[sl];
-          v[u] = (u64)svals[sl];
+  for (i64 fi = blockIdx.x; fi < hb.nfin; fi += gridDim.x) {
+    const int2 it = hb.fitem[fi];
+    const int h = it.x, b = it.y;
+    const int32_t r = a.rows[h];
+    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    HubPartial P;
+    P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1; P.sg = 0; P.pad = 0;
+    P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
+    if (MODE == M_MERGE && a.size[own] != 1) {  // CTA-uniform
+      if (threadIdx.x == 0) hb.part[fi] = P;
+      continue;
+    }
+    const i64 cf = hb.cfirst[h];
+    const int nch = hb.ccount[h];
+    for (int t0 = 0; t0 < nch; t0 += HUB_FIN_TILE) {
+      const int m = min(HUB_FIN_TILE, nch - t0);
+      for (int j = threadIdx.x; j < m; j += HUB_FIN_T) {
+        const i64 c = cf + t0 + j;
+        const int32_t *seg = hb.seg + hb.segoff[c];
+        const int s0 = seg[b], s1 = seg[b + 1];
+        tlen[j] = s1 - s0;
+        tst[j] = c * HUB_CHUNK + s0;
+      }
+      __syncthreads();
+      const int total = smem_excl_scan<HUB_FIN_T>(tlen, m);  // tlen[j] = prefix
+      for (int i = threadIdx.x; i < total; i += HUB_FIN_T) {
+        int lo = 0, hi = m - 1;  // last j with tlen[j] <= i
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (tlen[mid] <= i) lo = mid;
+          else hi = mid - 1;
+        }
+        const i64 e = tst[lo] + (i - tlen[lo]);
+        const int32_t k = hb.pkey[e];
+        const u64 v = hb.pval[e];
+        if (*(volatile int *)&scnt >= HUB_FIN_MAXD - 1) { sovf = 1; continue; }
+        bool claimed = false;
+        const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, HUB_FIN_LG, k, v, &claimed);
+        if (claimed) {
+          const int q = atomicAdd(&scnt, 1);
+          if (q < HUB_FIN_MAXD) slist[q] = (uint16_t)sl;
+          else sovf = 1;
         }
       }
+      __syncthreads();
+    }
+    if (sovf) {
+      if (threadIdx.x == 0) atomicOr(hb.overflow, 1);
+    }
+    const int n = min(scnt, HUB_FIN_MAXD);
+    if (MODE == M_SWEEP) {
+      const i64 di = a.delta[r];
+      constexpr int U = 4;
+      Cand best;
+      best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
+      u64 eown = 0, n1 = 0;
+      int32_t dm = 0;
+      for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
+        int32_t sl[U], k[U];
+        u64 v[U];
+        i64 dk[U];
 #pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u * HUB_FIN_T;
+          sl[u] = t < n ? (int32_t)slist[t] : -1;
+          k[u] = sl[u] >= 0 ? skeys[sl[u]] : -1;
+          v[u] = sl[u] >= 0 ? (u64)svals[sl[u]] : 0;
+          if (sl[u] >= 0) { skeys[sl[u]] = -1; svals[sl[u]] = 0; }
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
+        for (int u = 0; u < U; ++u)
+          dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (k[u] < 0) continue;
-        if (k[u] == own) {
-          eown = v[u];
-        } else {
-          ++n1;
-          const i128 S = move_score(a.twoW, v[u], di, dk[u]);
-          Cand x;
-          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
-          if (cand_better(x, best)) best = x;
+        for (int u = 0; u < U; ++u) {
+          if (k[u] < 0) continue;
+          if (k[u] == own) {
+            eown = v[u];
+          } else {
+            ++n1;
+            const i128 S = move_score(a.twoW, v[u], di, dk[u]);
+            Cand x;
+            x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
+            if (cand_better(x, best)) best = x;
+          }
         }
       }
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
+      if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
+    } else if (MODE == M_MERGE) {
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
+      u64 n1 = 0, unused = 0;
+      int32_t T = -1;
+      for (int i = threadIdx.x; i < n; i += HUB_FIN_T) {
+        const int sl = slist[i];
+        const int32_t k = skeys[sl];
+        skeys[sl] = -1;
+        svals[sl] = 0;
+        if (k != own) { ++n1; T = max(T, k); }
+      }
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
+      if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
+    } else {
+      u64 n1 = 0, selfw = 0, sumw = 0;
+      for (int i = threadIdx.x; i < n; i += HUB_FIN_T) {
+        const int sl = slist[i];
+        const int32_t k = skeys[sl];
+        const u64 v = (u64)svals[sl];
+        sumw += v;
+        if (k == r) selfw += v;
+        else ++n1;
+      }
+      u64 tot;
+      const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
+      if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
+      __syncthreads();
+      i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
+      for (int i = threadIdx.x; i < n; i += HUB_FIN_T) {
+        const int sl = slist[i];
+        const int32_t k = skeys[sl];
+        if (k != r && a.out_key) {
+          a.out_key[o] = k;
+          a.out_w[o] = (u64)svals[sl];
+          ++o;
+        }
+        skeys[sl] = -1;
+        svals[sl] = 0;
+      }
+      Cand none;
+      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
+      int32_t dm = 0;
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
+      if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
     }
-    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
-    if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.sg = best.sg; P.eown = eown; P.cnt = n1; }
-  } else if (MODE == M_MERGE) {
-    Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
-    u64 n1 = 0, unused = 0;
-    int32_t T = -1;
-    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
-      const int32_t k = skeys[slist[t]];
-      if (k != own) { ++n1; T = max(T, k); }
-    }
-    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
-    if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
-  } else {
-    u64 n1 = 0, selfw = 0, sumw = 0;
-    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
-      const int sl = slist[t];
-      const int32_t k = skeys[sl];
-      const u64 v = (u64)svals[sl];
-      sumw += v;
-      if (k == r) selfw += v;
-      else ++n1;
-    }
-    u64 tot;
-    const u64 pre = grp_excl_scan<HUB_FIN_T, HUB_FIN_T>(g, n1, tot);
-    __shared__ u64 sbase;
-    if (threadIdx.x == 0) sbase = atomicAdd(&hb.emit_cur[h], tot);
+    if (threadIdx.x == 0) hb.part[fi] = P;
     __syncthreads();
-    i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + (i64)(sbase + pre);
-    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
-      const int sl = slist[t];
-      const int32_t k = skeys[sl];
-      if (k != r && a.out_key) {
-        a.out_key[o] = k;
-        a.out_w[o] = (u64)svals[sl];
-        ++o;
-      }
-    }
-    Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
-    int32_t dm = 0;
-    grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
-    if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
+    if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) hb.part[blockIdx.x] = P;
 }
 
 template <int MODE>

@@ -345,6 +345,8 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.emit_cur = B.emit_cur.p;
     hb.overflow = B.overflow.p;
     hb.nhub = B.nhub;
+    hb.nchunks = B.nchunks;
+    hb.nfin = B.nfin;
     const size_t acc_smem = hub_acc_smem<VT>(B.max_blg);
     static size_t attr_acc = 0;
     static bool attr_fin = false;
@@ -358,10 +360,20 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
       attr_fin = true;
     }
     if (tm) tm->begin(hub_s, pre + "hub_acc");
-    LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)B.nchunks, HUB_ACC_T, acc_smem, a, hb);
+    static int occ_acc = -1, occ_fin = -1;
+    if (occ_acc < 0) {
+      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_acc, k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem));
+      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_hub_fin<MODE, VT>, HUB_FIN_T,
+                                                            hub_fin_smem<VT>()));
+      occ_acc = std::max(occ_acc, 1);
+      occ_fin = std::max(occ_fin, 1);
+    }
+    const i64 g_acc = std::min<i64>(B.nchunks, (i64)c.sms * occ_acc);
+    const i64 g_fin = std::min<i64>(B.nfin, (i64)c.sms * occ_fin);
+    LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)g_acc, HUB_ACC_T, acc_smem, a, hb);
     if (tm) tm->end(hub_s);
     if (tm) tm->begin(hub_s, pre + "hub_fin");
-    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)B.nfin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
+    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
     if (tm) tm->end(hub_s);
     if (tm) tm->begin(hub_s, pre + "hub_decide");
     LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
