@@ -72,6 +72,8 @@ struct AggArgs {
   const int32_t *label;    // snapshot labels C
   int32_t *label_next;     // decisions
   const i64 *deg;          // deg_C, indexed by label (snapshot)
+  const uint32_t *deg32;   // min(deg_C, 2^32-1): the gathered copy (half the bytes);
+                           // 0xFFFFFFFF means "read deg" (at most one community: Σ deg = 2W)
   const int32_t *size;     // |C|, indexed by label (snapshot)
   i64 *deg_next;           // SWEEP/MERGE: copy of deg receiving this pass's moves
   int32_t *size_next;      //   (P:L291 remove/insert; exact int64 atomics, order-free)
@@ -87,6 +89,12 @@ struct AggArgs {
   const Chunk *chunks;     // hub path: HUB_CHUNK-edge chunks of the hub rows
   int hint;                // bit0: evict_first on streams; bit1: evict_last on gathers
 };
+
+// deg_C through the 32-bit mirror (exact: saturated entries fall back to the 64-bit array)
+__device__ __forceinline__ i64 load_deg(const AggArgs &a, int32_t c) {
+  const uint32_t d = __ldg(&a.deg32[c]);
+  return d != 0xFFFFFFFFu ? (i64)d : __ldg(&a.deg[c]);
+}
 
 __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
   return ((uint32_t)k * 0x9E3779B1u) >> (32 - lg);
@@ -373,7 +381,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
 #pragma unroll
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
+        dk[u] = (k[u] >= 0 && k[u] != own) ? load_deg(a, k[u]) : 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (k[u] < 0) continue;
@@ -515,8 +523,8 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
     RowPre pre;
     if (MODE == M_SWEEP && g.lane == 0) {  // issued before the edge loop: overlaps it
-      pre.dq = __ldg(&a.deg[own]);
-      pre.dr = __ldg(&a.deg[r]);
+      pre.dq = load_deg(a, own);
+      pre.dr = load_deg(a, r);
       pre.szo = __ldg(&a.size[own]);
     }
     if (MODE == M_MERGE) {
@@ -544,8 +552,11 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
 // key are found with __match_any_sync and their weights summed (__reduce_add_sync when the
 // row sum fits 32 bits, else an exact shuffle loop); the first lane of each key group
 // stands for that candidate community.
+#ifndef LV_REG_MINB
+#define LV_REG_MINB 6  // CTAs of 256 per SM the register bins are compiled for (<= 42 regs)
+#endif
 template <int G, int BLOCK, int MODE, class WT, bool NARROW>
-__global__ void __launch_bounds__(BLOCK) k_agg_reg(AggArgs a) {
+__global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
   constexpr int GPB = BLOCK / G;
   Grp<G, BLOCK> g;
   const int grp = threadIdx.x / G;
@@ -567,8 +578,8 @@ __global__ void __launch_bounds__(BLOCK) k_agg_reg(AggArgs a) {
     if (MODE == M_SWEEP) {
       di = a.delta[r];
       if (g.lane == 0) {
-        dq = __ldg(&a.deg[own]);
-        dr = __ldg(&a.deg[r]);
+        dq = load_deg(a, own);
+        dr = load_deg(a, r);
         szo = __ldg(&a.size[own]);
       }
     }
@@ -623,7 +634,7 @@ __global__ void __launch_bounds__(BLOCK) k_agg_reg(AggArgs a) {
           eown = sum;
         } else {
           ncand = 1;
-          const i64 dk = (a.hint & 2) ? ld_keep(&a.deg[k], l2_policy_last()) : __ldg(&a.deg[k]);
+          const i64 dk = load_deg(a, k);
           const i128 S = move_score(a.twoW, sum, di, dk);
           best.hi = (i64)(S >> 64); best.lo = (u64)S; best.c = k;
         }
@@ -688,16 +699,16 @@ __global__ void __launch_bounds__(BLOCK) k_agg_reg(AggArgs a) {
 //                chunk's pool region grouped by bucket, with the bucket boundaries in
 //                the chunk's segment table.  Sequential writes only.
 //   k_hub_fin    one CTA per (row, bucket): merge that bucket's segments of every chunk
-//                of the row in a shared table (expected <= 2048 distinct keys), then score
+//                of the row in a shared table (expected <= 1024 distinct keys), then score
 //                / count / emit them and write one partial.
 //   k_hub_decide one thread per row: combine the row's partials and decide.
 constexpr i64 HUB_CHUNK = 4096;
 constexpr int HUB_ACC_T = 512;
 constexpr int HUB_SM_LG = 13;      // chunk table: 8192 slots >= 2 x 4096 distinct (exact bound)
 constexpr int HUB_FIN_T = 256;
-constexpr int HUB_FIN_LG = 13;     // bucket table: 8192 slots
-constexpr int HUB_FIN_MAXD = 4096; // distinct keys allowed per bucket (load <= 0.5); expected <= 2048
-constexpr i64 HUB_BUCKET_TARGET = 2048;
+constexpr int HUB_FIN_LG = 12;     // bucket table: 4096 slots
+constexpr int HUB_FIN_MAXD = 2048; // distinct keys allowed per bucket (load <= 0.5); expected <= 1024
+constexpr i64 HUB_BUCKET_TARGET = 1024;
 constexpr int HUB_MAX_BLG = 15;    // <= 32768 buckets per row (histogram sized per launch)
 constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
 
@@ -911,7 +922,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          dk[u] = (k[u] >= 0 && k[u] != own) ? ((a.hint & 2) ? ld_keep(&a.deg[k[u]], l2_policy_last()) : __ldg(&a.deg[k[u]])) : 0;
+          dk[u] = (k[u] >= 0 && k[u] != own) ? load_deg(a, k[u]) : 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (k[u] < 0) continue;
@@ -1003,7 +1014,7 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     }
     if (MODE == M_SWEEP) {
       const i64 di = a.delta[r];
-      const i64 dq = a.deg[own];
+      const i64 dq = load_deg(a, own);
       i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
       int32_t tgt = own;
       if (best.c != INT32_MAX && cand_S(best) > S_own) {
@@ -1015,7 +1026,7 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
       acc.moved += (tgt != own);
       acc.i2 += eown;
       acc.cand += cnt;
-      acc.add_sq(a.deg[r]);
+      acc.add_sq(load_deg(a, r));
     } else if (MODE == M_MERGE) {
       int32_t tgt = own;
       if (a.size[own] == 1 && cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
@@ -1046,6 +1057,14 @@ __global__ void __launch_bounds__(256) k_apply_moves(i64 n, const int32_t *__res
       atomicSub(&size_next[a], 1);
       atomicAdd(&size_next[b], 1);
     }
+  }
+}
+
+// deg32[c] = min(deg[c], 2^32 - 1) (the gathered mirror of deg_C)
+__global__ void __launch_bounds__(256) k_deg32(i64 n, const i64 *__restrict__ deg, uint32_t *deg32) {
+  for (i64 c = (i64)blockIdx.x * 256 + threadIdx.x; c < n; c += (i64)gridDim.x * 256) {
+    const i64 d = deg[c];
+    deg32[c] = d >= (i64)0xFFFFFFFF ? 0xFFFFFFFFu : (uint32_t)d;
   }
 }
 

@@ -222,6 +222,7 @@ namespace {
 struct State {
   Buf<int32_t> lab[2];
   Buf<i64> deg[2];
+  Buf<uint32_t> deg32[2];  // saturating 32-bit mirror of deg (what the kernels gather)
   Buf<int32_t> size[2];
   int cur = 0;
 };
@@ -304,6 +305,7 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   a.label = st.lab[st.cur].p;
   a.label_next = st.lab[st.cur ^ 1].p;
   a.deg = st.deg[st.cur].p;
+  a.deg32 = st.deg32[st.cur].p;
   a.size = st.size[st.cur].p;
   i64 *deg_next = st.deg[st.cur ^ 1].p;
   int32_t *size_next = st.size[st.cur ^ 1].p;
@@ -353,6 +355,7 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   }
   if (P.sharded)  // identical on every rank: apply all moves to the next-state deg/size
     LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, a.label, a.label_next, g.delta.p, deg_next, size_next);
+  LV_LAUNCH(c, k_deg32, grid_for(c, g.n), 256, 0, g.n, deg_next, st.deg32[st.cur ^ 1].p);
   if (tm && mode == M_SWEEP) tm->end(c.s);
   LV_CUDA(cudaMemcpyAsync(h->hctr, src, (size_t)nsum * SLOT * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
@@ -413,11 +416,13 @@ void init_state(louvain_ctx *h, const DGraph &g, State &st) {
   for (int b = 0; b < 2; ++b) {
     st.lab[b].alloc(c.A, g.n);
     st.deg[b].alloc(c.A, g.n);
+    st.deg32[b].alloc(c.A, g.n);
     st.size[b].alloc(c.A, g.n);
   }
   st.cur = 0;
   LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg[0].p, st.size[0].p,
             g.delta.p);
+  LV_LAUNCH(c, k_deg32, grid_for(c, g.n), 256, 0, g.n, st.deg[0].p, st.deg32[0].p);
 }
 
 // Level constants: Σ loop and Σ_{inactive} δ² (labels of vertices without neighbours
@@ -763,6 +768,7 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     for (int b = 0; b < 2; ++b) {
       st.lab[b].alloc(c.A, n);
       st.deg[b].alloc(c.A, n);
+      st.deg32[b].alloc(c.A, n);
       st.size[b].alloc(c.A, n);
     }
     LV_CUDA(cudaMemcpyAsync(st.lab[0].p, labels_in, n * sizeof(int32_t),
@@ -774,6 +780,7 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
     LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg[0].p, st.size[0].p,
               err.p);
+    LV_LAUNCH(c, k_deg32, grid_for(c, n), 256, 0, n, st.deg[0].p, st.deg32[0].p);
     int herr = 0;
     LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
