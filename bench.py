@@ -270,19 +270,23 @@ def main():
     t_ms, t_bytes, t_launch = agg[top] if agg else (float("nan"), float("nan"), 1.0)
     achieved = t_bytes / (t_ms / 1e3) / 1e9
     sweep_ms = (sweep_pass[0] / args.steps) if sweep_pass else None
-    traffic = None
+    traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # DRAM bytes of one ncu --set full capture of this kernel
         try:
-            traffic = json.load(open(tf)).get(args.workload, {}).get(top)
+            t = json.load(open(tf)).get(args.workload, {}).get(top)
+            if t:
+                traffic = t["bytes"]
+                traffic_note = (f"{t['launch']}; that launch's algorithmic bytes: {t['alg_bytes_same_launch']:.4g} "
+                                f"(traffic/algorithmic = {t['bytes'] / t['alg_bytes_same_launch']:.2f})")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": top,
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note, "kernel": top,
                 "kernel_ms_per_launch": t_ms / t_launch, "alg_bytes_per_launch": t_bytes / t_launch,
                 "kernel_share_of_step": t_ms / args.steps / ms, "peak_source": pk["source"],
-                "note": "bin kernels run concurrently on side streams; per-kernel times are CUDA events on "
-                        "each kernel's own stream"}
+                "note": "per-kernel times: CUDA events on each kernel's launching stream over the timed steps; "
+                        "achieved = algorithmic bytes (DESIGN.md §6) / time, averaged over all levels' launches"}
     sweep_roof = None
     if sweep_pass:
         sp_ms, sp_bytes, sp_n = sweep_pass
