@@ -198,6 +198,7 @@ struct louvain_ctx {
   bool shard = false;
   int world = 1, rank = 0, sim = 0;
   void *comm = nullptr;
+  bool compact = true;         // LV_NO_COMPACT=1 disables the per-level compaction
   int l2mode = 1;              // LV_L2MODE: bit0 evict_first streams (default), bit1 evict_last
                                // gathers, bit2 persisting L2 window on the snapshot labels
   size_t l2win = 0;
@@ -442,12 +443,10 @@ void level_consts(louvain_ctx *h, const DGraph &g, u64 &lsum, u128 &s2_inact) {
 }
 
 // Algorithm 1 for one level.  Returns the number of committed sweeps.
-int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, double theta) {
+// lsum = Σ loop and s2i = Σ_{inactive} δ² of the level (of the uncompacted graph).
+int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, double theta, u64 lsum, u128 s2i) {
   const louvain_config &cfg = h->cfg;
   if (cfg.max_sweeps <= 0) return 0;
-  u64 lsum;
-  u128 s2i;
-  level_consts(h, g, lsum, s2i);
   const bool prof = cfg.profile != 0 && !P.sharded;
   const Bins &B = *P.parts[0];
   KTimer tm;
@@ -515,26 +514,60 @@ void run_impl(louvain_ctx *h) {
     rec->n = g->n;
     rec->times[0] = l == 0 ? h->csr_ms : 0.0;
     double t0 = now_ms();
+    u64 lsum;
+    u128 s2i;
+    level_consts(h, *g, lsum, s2i);
+    // sweep on the order-preserving compaction of g when many vertices are isolated
+    DGraph gc;
+    Compaction cp;
+    const bool compacted = h->compact && compact_graph(c, *g, 0.9, gc, cp);
+    const DGraph &gs = compacted ? gc : *g;
     State st;
-    init_state(h, *g, st);
-    Plan P = make_plan(h, *g);
+    init_state(h, gs, st);
+    Plan P = make_plan(h, gs);
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t1 = now_ms();
-    rec->sweeps = one_level(h, *g, P, st, theta);
+    rec->sweeps = one_level(h, gs, P, st, theta, lsum, s2i);
     if (cfg.merge_isolated) {
-      run_pass(h, *g, P, st, M_MERGE);
-      commit(h, *g, st);
+      run_pass(h, gs, P, st, M_MERGE);
+      commit(h, gs, st);
+    }
+    const int32_t *lab_f = st.lab[st.cur].p;
+    const int32_t *size_f = st.size[st.cur].p;
+    const i64 *deg_f = st.deg[st.cur].p;
+    Buf<int32_t> lab_o, size_o;
+    Buf<i64> deg_o;
+    if (compacted) {  // back to g's index space
+      lab_o.alloc(c.A, g->n);
+      size_o.alloc(c.A, g->n);
+      deg_o.alloc(c.A, g->n);
+      LV_LAUNCH(c, k_expand_state, grid_for(c, g->n), 256, 0, g->n, g->row_ptr.p, cp.m.p, cp.inv.p, lab_f, size_f, deg_f,
+                g->delta.p, lab_o.p, size_o.p, deg_o.p);
+      lab_f = lab_o.p;
+      size_f = size_o.p;
+      deg_f = deg_o.p;
     }
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t2 = now_ms();
     rec->labels.alloc(c.A, g->n);
     Buf<i64> ndelta;
-    const i64 k = renumber(c, g->n, st.lab[st.cur].p, st.size[st.cur].p, st.deg[st.cur].p, rec->labels.p, ndelta);
+    const i64 k = renumber(c, g->n, lab_f, size_f, deg_f, rec->labels.p, ndelta);
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t3 = now_ms();
     st = State();
+    lab_o.release();
+    size_o.release();
+    deg_o.release();
     auto hg = std::make_unique<DGraph>();
-    contract(c, *g, P.all(c, *g), rec->labels.p, k, std::move(ndelta), *hg);
+    if (compacted) {
+      P = Plan();
+      gc = DGraph();
+      Bins Bg;  // contraction runs on g itself
+      build_bins(c, g->row_ptr.p, g->n, g->n, Bg);
+      contract(c, *g, Bg, rec->labels.p, k, std::move(ndelta), *hg);
+    } else {
+      contract(c, *g, P.all(c, *g), rec->labels.p, k, std::move(ndelta), *hg);
+    }
     double t4 = now_ms();
     rec->q = q_of_contracted(h, *hg);
     rec->times[1] = t1 - t0;
@@ -626,7 +659,8 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       LV_CUDA(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
       h->own_stream = true;
     }
-    if (getenv("LV_CONCURRENT")) h->c.init_side();  // degree bins on side streams (measured slower)
+    if (getenv("LV_CONCURRENT")) h->c.init_side();
+    if (getenv("LV_NO_COMPACT")) h->compact = false;  // degree bins on side streams (measured slower)
     h->c.A.a = cfg.alloc;
     h->c.A.f = cfg.free;
     h->c.A.ctx = cfg.alloc_ctx;
@@ -821,8 +855,13 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
   try {
     Ctx &c = h->c;
     LV_CUDA(cudaSetDevice(c.device));
-    const DGraph &g = h->g0;
-    Bins &B = vbins0(h);
+    DGraph gc;  // sweep what louvain_run sweeps: the compacted level-0 graph when it applies
+    Compaction cp;
+    const bool compacted = h->compact && compact_graph(c, h->g0, 0.9, gc, cp);
+    const DGraph &g = compacted ? gc : h->g0;
+    Bins Bc;
+    if (compacted) build_bins(c, g.row_ptr.p, g.n, g.n, Bc);
+    Bins &B = compacted ? Bc : vbins0(h);
     State st;
     init_state(h, g, st);
     const Plan PL = plan_of(B);
@@ -857,6 +896,7 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
     std::string js = "{\"ms_sweep\": " + std::to_string(total_ms / reps) +
                      ", \"alg_bytes_sweep\": " + std::to_string(alg / reps) +
                      ", \"edges\": " + std::to_string(g.nnz) + ", \"n\": " + std::to_string(g.n) +
+                     ", \"compacted\": " + (compacted ? std::string("true") : std::string("false")) +
                      ", \"active\": " + std::to_string(B.active()) + ", \"kernels\": " + P.json(reps) + "}";
     if ((int64_t)js.size() + 1 > cap) return LV_EINVAL;
     memcpy(json, js.c_str(), js.size() + 1);

@@ -447,4 +447,89 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   LV_CUDA(cudaStreamSynchronize(c.s));
 }
 
+// ------------------------------------------------------------------ compaction
+// Order-preserving removal of vertices without non-loop neighbours from a level graph
+// (they never move and are never gathered).  m[v] = rank of v among the active vertices
+// is monotone, so every label comparison the method makes (min-label ties, the singlet
+// rule, the order-preserving renumbering) is unchanged on the compacted graph, while the
+// gathered label / deg_C arrays shrink to the active vertices (locality in L2).
+struct ActiveFlag {
+  const i64 *rp;
+  __device__ __forceinline__ i64 operator()(i64 v) const { return rp[v + 1] > rp[v] ? 1 : 0; }
+};
+
+__global__ void k_compact_build(i64 n, const i64 *__restrict__ rp, const i64 *__restrict__ delta,
+                                const i64 *__restrict__ loop, const i64 *__restrict__ m, int32_t *inv, i64 *rp_c,
+                                i64 *delta_c, i64 *loop_c) {
+  for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256) {
+    if (rp[v + 1] > rp[v]) {
+      const i64 i = m[v];
+      inv[i] = (int32_t)v;
+      rp_c[i] = rp[v];
+      delta_c[i] = delta[v];
+      loop_c[i] = loop[v];
+    }
+  }
+}
+
+__global__ void k_remap_col(i64 nnz, const int32_t *__restrict__ col, const i64 *__restrict__ m, int32_t *col_c) {
+  for (i64 e = (i64)blockIdx.x * 256 + threadIdx.x; e < nnz; e += (i64)gridDim.x * 256) col_c[e] = (int32_t)m[col[e]];
+}
+
+// Back to the original index space: labels (compacted community ids -> original vertex
+// ids) and per-community size / deg (indexed by the original label).
+__global__ void k_expand_state(i64 n, const i64 *__restrict__ rp, const i64 *__restrict__ m,
+                               const int32_t *__restrict__ inv, const int32_t *__restrict__ lab_c,
+                               const int32_t *__restrict__ size_c, const i64 *__restrict__ deg_c,
+                               const i64 *__restrict__ delta, int32_t *lab_o, int32_t *size_o, i64 *deg_o) {
+  for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256) {
+    if (rp[v + 1] > rp[v]) {
+      const i64 i = m[v];
+      lab_o[v] = inv[lab_c[i]];
+      size_o[v] = size_c[i];
+      deg_o[v] = deg_c[i];
+    } else {
+      lab_o[v] = (int32_t)v;
+      size_o[v] = 1;
+      deg_o[v] = delta[v];
+    }
+  }
+}
+
+struct Compaction {
+  i64 na = 0;
+  Buf<i64> m;
+  Buf<int32_t> inv;
+};
+
+// Builds gc (the compacted level graph) if the active fraction is below `max_frac`.
+inline bool compact_graph(Ctx &c, const DGraph &g, double max_frac, DGraph &gc, Compaction &cp) {
+  cp.m.alloc(c.A, g.n + 1);
+  exclusive_scan<i64>(c, ActiveFlag{g.row_ptr.p}, g.n, cp.m.p, true);
+  cp.na = d2h_i64(c, cp.m.p + g.n);
+  if (cp.na == 0 || (double)cp.na > max_frac * (double)g.n) {
+    cp.m.release();
+    return false;
+  }
+  const i64 na = cp.na;
+  cp.inv.alloc(c.A, na);
+  gc.n = na;
+  gc.nnz = g.nnz;
+  gc.W = g.W;
+  gc.wt = g.wt;
+  gc.max_delta = g.max_delta;
+  gc.row_ptr.alloc(c.A, na + 1);
+  gc.delta.alloc(c.A, na);
+  gc.loop.alloc(c.A, na);
+  gc.col.alloc(c.A, g.nnz > 0 ? g.nnz : 1);
+  gc.w.alloc(c.A, g.nnz * (i64)wbytes(g.wt) + 8);
+  LV_LAUNCH(c, k_compact_build, grid_for(c, g.n), 256, 0, g.n, g.row_ptr.p, g.delta.p, g.loop.p, cp.m.p, cp.inv.p,
+            gc.row_ptr.p, gc.delta.p, gc.loop.p);
+  LV_CUDA(cudaMemcpyAsync(gc.row_ptr.p + na, g.row_ptr.p + g.n, sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
+  LV_LAUNCH(c, k_remap_col, grid_for(c, g.nnz), 256, 0, g.nnz, g.col.p, cp.m.p, gc.col.p);
+  if (g.wt != WT_NONE)
+    LV_CUDA(cudaMemcpyAsync(gc.w.p, g.w.p, g.nnz * (i64)wbytes(g.wt), cudaMemcpyDeviceToDevice, c.s));
+  return true;
+}
+
 }  // namespace lv
