@@ -81,7 +81,9 @@ struct AggArgs {
   i64 twoW;                // 2W
   const i64 *out_base;     // EMIT: output offset of row r (NULL -> ptr)
   int32_t *out_key;        // EMIT outputs (NULL -> count only)
-  u64 *out_w;
+  void *out_w;             // weights of the emitted entries: u64, or uint32 when out_w32
+  int out_w32;             // 1: out_w holds uint32 (the destination CSR's weight type)
+  int out_wnone;           // 1: the destination CSR is unweighted (weights not written)
   i64 *out_cnt;            // distinct keys ≠ row id
   u64 *out_self;           // Σ w with key == row id (may be NULL)
   u64 *out_sum;            // Σ w over the row (may be NULL)
@@ -89,6 +91,12 @@ struct AggArgs {
   const Chunk *chunks;     // hub path: HUB_CHUNK-edge chunks of the hub rows
   int hint;                // bit0: evict_first on streams; bit1: evict_last on gathers
 };
+
+__device__ __forceinline__ void store_w(const AggArgs &a, i64 o, u64 v) {
+  if (a.out_wnone) return;
+  if (a.out_w32) ((uint32_t *)a.out_w)[o] = (uint32_t)v;
+  else ((u64 *)a.out_w)[o] = v;
+}
 
 // deg_C through the 32-bit mirror (exact: saturated entries fall back to the 64-bit array)
 __device__ __forceinline__ i64 load_deg(const AggArgs &a, int32_t c) {
@@ -457,7 +465,7 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         vals[sl] = 0;
         if (k != r && a.out_key) {
           a.out_key[o] = k;
-          a.out_w[o] = v;
+          store_w(a, o, v);
           ++o;
         }
       }
@@ -673,7 +681,7 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
       if (emit && a.out_key) {
         const i64 o = (a.out_base ? a.out_base[r] : a.ptr[r]) + __popc(bal & ((1u << wl) - 1u));
         a.out_key[o] = k;
-        a.out_w[o] = sum;
+        store_w(a, o, sum);
       }
       Cand none;
       none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
@@ -706,8 +714,10 @@ constexpr i64 HUB_CHUNK = 4096;
 constexpr int HUB_ACC_T = 512;
 constexpr int HUB_SM_LG = 13;      // chunk table: 8192 slots >= 2 x 4096 distinct (exact bound)
 constexpr int HUB_FIN_T = 256;
-constexpr int HUB_FIN_LG = 12;     // bucket table: 4096 slots
-constexpr int HUB_FIN_MAXD = 2048; // distinct keys allowed per bucket (load <= 0.5); expected <= 1024
+// bucket table: 2^fin_lg slots, <= 2^(fin_lg-1) distinct keys (load <= 0.5), buckets sized
+// for an expected 2^(fin_lg-2); fin_lg = 12 normally, up to 14 (per launch) for giant rows
+constexpr int HUB_FIN_LG = 12;
+constexpr int HUB_FIN_LG_MAX = 14;
 constexpr i64 HUB_BUCKET_TARGET = 1024;
 constexpr int HUB_MAX_BLG = 15;    // <= 32768 buckets per row (histogram sized per launch)
 constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
@@ -735,8 +745,9 @@ struct HubArgs {
   const int2 *fitem;      // per fin item: (hub, bucket)
   HubPartial *part;       // per fin item
   u64 *emit_cur;          // per hub (EMIT output cursor)
-  int *overflow;          // set if a bucket exceeds HUB_FIN_MAXD distinct keys
+  int *overflow;          // set if a bucket exceeds its distinct-key capacity
   i64 nhub, nchunks, nfin;
+  int fin_lg;             // bucket table log2 capacity of this launch
 };
 
 template <class VT>
@@ -745,8 +756,8 @@ constexpr size_t hub_acc_smem(int max_blg) {
          (size_t)((1 << max_blg) + 1) * sizeof(int) + 64;
 }
 template <class VT>
-constexpr size_t hub_fin_smem() {
-  return (size_t)(1 << HUB_FIN_LG) * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_FIN_MAXD * sizeof(uint16_t) +
+constexpr size_t hub_fin_smem(int fin_lg) {
+  return ((size_t)1 << fin_lg) * (sizeof(VT) + sizeof(int32_t)) + ((size_t)1 << (fin_lg - 1)) * sizeof(uint16_t) +
          (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
 }
 
@@ -839,11 +850,13 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
 template <int MODE, class VT>
 __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   extern __shared__ __align__(16) unsigned char sm[];
-  constexpr int CAPF = 1 << HUB_FIN_LG;
+  const int FLG = hb.fin_lg;
+  const int CAPF = 1 << FLG;
+  const int MAXD = CAPF / 2;
   VT *svals = (VT *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)CAPF * sizeof(VT));
   uint16_t *slist = (uint16_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
-  i64 *tst = (i64 *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_FIN_MAXD * sizeof(uint16_t));
+  i64 *tst = (i64 *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)) + (size_t)MAXD * sizeof(uint16_t));
   int *tlen = (int *)(tst + HUB_FIN_TILE);
   __shared__ int scnt, sovf;
   __shared__ u64 sbase;
@@ -886,12 +899,12 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         const i64 e = tst[lo] + (i - tlen[lo]);
         const int32_t k = hb.pkey[e];
         const u64 v = hb.pval[e];
-        if (*(volatile int *)&scnt >= HUB_FIN_MAXD - 1) { sovf = 1; continue; }
+        if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
         bool claimed = false;
-        const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, HUB_FIN_LG, k, v, &claimed);
+        const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, FLG, k, v, &claimed);
         if (claimed) {
           const int q = atomicAdd(&scnt, 1);
-          if (q < HUB_FIN_MAXD) slist[q] = (uint16_t)sl;
+          if (q < MAXD) slist[q] = (uint16_t)sl;
           else sovf = 1;
         }
       }
@@ -900,7 +913,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     if (sovf) {
       if (threadIdx.x == 0) atomicOr(hb.overflow, 1);
     }
-    const int n = min(scnt, HUB_FIN_MAXD);
+    const int n = min(scnt, MAXD);
     if (MODE == M_SWEEP) {
       const i64 di = a.delta[r];
       constexpr int U = 4;
@@ -973,7 +986,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         const int32_t k = skeys[sl];
         if (k != r && a.out_key) {
           a.out_key[o] = k;
-          a.out_w[o] = (u64)svals[sl];
+          store_w(a, o, (u64)svals[sl]);
           ++o;
         }
         skeys[sl] = -1;

@@ -661,6 +661,12 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
     }
     if (getenv("LV_CONCURRENT")) h->c.init_side();
     if (getenv("LV_NO_COMPACT")) h->compact = false;  // degree bins on side streams (measured slower)
+    if (!cfg.alloc) {  // keep freed blocks in the stream-ordered pool (no release on sync)
+      cudaMemPool_t pool;
+      LV_CUDA(cudaDeviceGetDefaultMemPool(&pool, cfg.device));
+      uint64_t thr = UINT64_MAX;
+      LV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     h->c.A.a = cfg.alloc;
     h->c.A.f = cfg.free;
     h->c.A.ctx = cfg.alloc_ctx;

@@ -74,6 +74,7 @@ struct Bins {
   // hub path (see lv_agg.cuh): chunks, buckets, pool, segment tables, partials
   i64 nhub = 0, nchunks = 0, nfin = 0, nseg = 0;
   int max_blg = 0;
+  int fin_lg = HUB_FIN_LG;
   Buf<Chunk> chunks;
   Buf<i64> cfirst, bfirst, segoff;
   Buf<int32_t> ccount, blg, seg, pkey;
@@ -210,9 +211,15 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     std::vector<int32_t> ccount(B.nhub), blg(B.nhub);
     std::vector<Chunk> ch;
     std::vector<int2> fit;
+    // bucket table size: the smallest fin_lg whose buckets (<= 2^HUB_MAX_BLG per row) can
+    // hold every hub row's distinct keys at the expected load
+    i64 dmax = 0;
+    for (i64 h = 0; h < B.nhub; ++h) dmax = std::max(dmax, std::min(len[h], universe));
+    B.fin_lg = HUB_FIN_LG;
+    while (B.fin_lg < HUB_FIN_LG_MAX && ((i64)1 << (B.fin_lg - 2 + HUB_MAX_BLG)) < dmax) ++B.fin_lg;
     // LV_HUB_BUCKET_TARGET (tests only) shrinks the bucket target to exercise many buckets
-    static const i64 target = getenv("LV_HUB_BUCKET_TARGET") ? atoll(getenv("LV_HUB_BUCKET_TARGET"))
-                                                              : HUB_BUCKET_TARGET;
+    static const char *tenv = getenv("LV_HUB_BUCKET_TARGET");
+    const i64 target = tenv ? atoll(tenv) : ((i64)1 << (B.fin_lg - 2));
     for (i64 h = 0; h < B.nhub; ++h) {
       const i64 distinct_max = std::min(len[h], universe);
       int lgb = 0;
@@ -347,24 +354,25 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.nhub = B.nhub;
     hb.nchunks = B.nchunks;
     hb.nfin = B.nfin;
+    hb.fin_lg = B.fin_lg;
     const size_t acc_smem = hub_acc_smem<VT>(B.max_blg);
     static size_t attr_acc = 0;
-    static bool attr_fin = false;
+    static size_t attr_fin = 0;
+    const size_t fin_smem = hub_fin_smem<VT>(B.fin_lg);
     if (acc_smem > attr_acc) {
       LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
       attr_acc = acc_smem;
     }
-    if (!attr_fin) {
-      LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)hub_fin_smem<VT>()));
-      attr_fin = true;
+    if (fin_smem > attr_fin) {
+      LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem));
+      attr_fin = fin_smem;
     }
     if (tm) tm->begin(hub_s, pre + "hub_acc");
     static int occ_acc = -1, occ_fin = -1;
     if (occ_acc < 0) {
       LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_acc, k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem));
       LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_hub_fin<MODE, VT>, HUB_FIN_T,
-                                                            hub_fin_smem<VT>()));
+                                                            hub_fin_smem<VT>(HUB_FIN_LG)));
       occ_acc = std::max(occ_acc, 1);
       occ_fin = std::max(occ_fin, 1);
     }
@@ -373,7 +381,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)g_acc, HUB_ACC_T, acc_smem, a, hb);
     if (tm) tm->end(hub_s);
     if (tm) tm->begin(hub_s, pre + "hub_fin");
-    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, hub_fin_smem<VT>(), a, hb);
+    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
     if (tm) tm->end(hub_s);
     if (tm) tm->begin(hub_s, pre + "hub_decide");
     LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
@@ -395,7 +403,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
       LV_CUDA(cudaStreamWaitEvent(c.s, c.join_ev[i], 0));
     }
   }
-  if (B.nhub) {  // a bucket beyond HUB_FIN_MAXD distinct keys would have been dropped
+  if (B.nhub) {  // a bucket beyond its distinct-key capacity would have been dropped
     int ovf = 0;
     LV_CUDA(cudaMemcpyAsync(&ovf, B.overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));

@@ -4,6 +4,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -49,16 +51,38 @@ struct Alloc {
     void *p = nullptr;
     if (a) {
       p = a(ctx, bytes, (void *)s);
-      LV_REQUIRE(p != nullptr, LV_ENOMEM, "device allocation hook failed (" + std::to_string(bytes) + " B)");
+      if (!p) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        throw Error{LV_ENOMEM, "device allocation hook failed (" + std::to_string(bytes) + " B; library live " +
+                                   std::to_string(live) + " B, peak " + std::to_string(peak) + " B; device free " +
+                                   std::to_string(fr) + " of " + std::to_string(tot) + " B)"};
+      }
     } else {
       cudaError_t e = cudaMallocAsync(&p, bytes, s);
+      if (e != cudaSuccess) {  // freed blocks may be fragmented in the pool: trim it, retry once
+        cudaGetLastError();
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        cudaStreamSynchronize(s);
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync(&p, bytes, s);
+      }
       if (e != cudaSuccess) {
         cudaGetLastError();
-        throw Error{LV_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e)};
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        throw Error{LV_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e) +
+                                   " (library live " + std::to_string(live) + " B, peak " + std::to_string(peak) +
+                                   " B; device free " + std::to_string(fr) + " of " + std::to_string(tot) + " B)"};
       }
     }
     live += bytes;
     if (live > peak) peak = live;
+    static const bool trace = getenv("LV_TRACE_ALLOC") != nullptr;
+    if (trace && bytes >= ((size_t)256 << 20))
+      fprintf(stderr, "[lv alloc] %.2f GB -> live %.2f GB\n", bytes / 1e9, live / 1e9);
     return p;
   }
   void put(void *p, size_t bytes) {
@@ -66,6 +90,9 @@ struct Alloc {
     if (bytes == 0) bytes = 16;
     bytes = (bytes + 255) & ~size_t(255);
     live -= bytes;
+    static const bool trace = getenv("LV_TRACE_ALLOC") != nullptr;
+    if (trace && bytes >= ((size_t)256 << 20))
+      fprintf(stderr, "[lv free ] %.2f GB -> live %.2f GB\n", bytes / 1e9, live / 1e9);
     if (f) f(ctx, p, bytes, (void *)s);
     else cudaFreeAsync(p, s);
   }

@@ -85,73 +85,6 @@ __global__ void __launch_bounds__(256) k_coo_fill(i64 m, const int32_t *__restri
   }
 }
 
-// Copy each row's first cnt[r] entries (keys + u64 weights) from src_base[r] to
-// dst_ptr[r], converting the weight to WOUT.  One group of G lanes per row.
-template <int G, int BLOCK, class WOUT>
-__global__ void __launch_bounds__(BLOCK) k_copy_rows(const int32_t *__restrict__ rows, i64 nrows,
-                                                     const i64 *__restrict__ src_base, const i64 *__restrict__ cnt,
-                                                     const i64 *__restrict__ dst_ptr, const int32_t *__restrict__ skey,
-                                                     const u64 *__restrict__ sw, int32_t *dkey, void *dw) {
-  constexpr int GPB = BLOCK / G;
-  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
-  for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < nrows; idx += (i64)gridDim.x * GPB) {
-    const int32_t r = rows[idx];
-    const i64 s = src_base[r], d = dst_ptr[r], c = cnt[r];
-    for (i64 t = lane; t < c; t += G) {
-      dkey[d + t] = skey[s + t];
-      if (WOUT::bytes == 4) ((uint32_t *)dw)[d + t] = (uint32_t)sw[s + t];
-      if (WOUT::bytes == 8) ((u64 *)dw)[d + t] = sw[s + t];
-    }
-  }
-}
-
-// Hub rows: chunked copy (chunks cover the row's source range; copy the part < cnt).
-template <class WOUT>
-__global__ void __launch_bounds__(256) k_copy_hub(const Chunk *__restrict__ chunks, const int32_t *__restrict__ rows,
-                                                  const i64 *__restrict__ src_base, const i64 *__restrict__ cnt,
-                                                  const i64 *__restrict__ dst_ptr, const int32_t *__restrict__ skey,
-                                                  const u64 *__restrict__ sw, int32_t *dkey, void *dw) {
-  const Chunk ch = chunks[blockIdx.x];
-  const int32_t r = rows[ch.h];
-  const i64 s = src_base[r], d = dst_ptr[r], c = cnt[r];
-  const i64 t0 = ch.beg - s, t1 = min(ch.end - s, c);
-  for (i64 t = t0 + threadIdx.x; t < t1; t += 256) {
-    dkey[d + t] = skey[s + t];
-    if (WOUT::bytes == 4) ((uint32_t *)dw)[d + t] = (uint32_t)sw[s + t];
-    if (WOUT::bytes == 8) ((u64 *)dw)[d + t] = sw[s + t];
-  }
-}
-
-template <class WOUT>
-void copy_rows_t(Ctx &c, const Bins &B, const i64 *src_base, const i64 *cnt, const i64 *dst_ptr,
-                 const int32_t *skey, const u64 *sw, int32_t *dkey, void *dw) {
-  auto one = [&](int b, auto kern, int GPB, int BLOCK) {
-    if (!B.count(b)) return;
-    i64 grid = cdiv(B.count(b), GPB);
-    if (grid > (i64)c.sms * 16) grid = (i64)c.sms * 16;
-    LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, 0, B.rows.p + B.off[b], B.count(b), src_base, cnt, dst_ptr, skey, sw,
-              dkey, dw);
-  };
-  one(0, k_copy_rows<4, 256, WOUT>, 64, 256);
-  one(1, k_copy_rows<8, 256, WOUT>, 32, 256);
-  one(2, k_copy_rows<16, 256, WOUT>, 16, 256);
-  one(3, k_copy_rows<32, 256, WOUT>, 8, 256);
-  one(4, k_copy_rows<32, 256, WOUT>, 8, 256);
-  one(5, k_copy_rows<128, 256, WOUT>, 2, 256);
-  one(6, k_copy_rows<256, 256, WOUT>, 1, 256);
-  one(7, k_copy_rows<256, 256, WOUT>, 1, 256);
-  if (B.nhub)
-    LV_LAUNCH(c, k_copy_hub<WOUT>, (unsigned)B.nchunks, 256, 0, B.chunks.p, B.rows.p + B.off[NSMEM], src_base, cnt,
-              dst_ptr, skey, sw, dkey, dw);
-}
-
-inline void copy_rows(Ctx &c, int wt, const Bins &B, const i64 *src_base, const i64 *cnt, const i64 *dst_ptr,
-                      const int32_t *skey, const u64 *sw, int32_t *dkey, void *dw) {
-  if (wt == WT_NONE) copy_rows_t<WNone>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
-  else if (wt == WT_U32) copy_rows_t<WU32>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
-  else copy_rows_t<WU64>(c, B, src_base, cnt, dst_ptr, skey, sw, dkey, dw);
-}
-
 __global__ void k_delta(i64 n, const u64 *__restrict__ rowsum, const i64 *__restrict__ loop, i64 *delta) {
   for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256)
     delta[i] = (i64)rowsum[i] + 2 * loop[i];
@@ -222,11 +155,10 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
     else LV_LAUNCH(c, (k_coo_fill<RI64, WU64>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
   }
   cnt.release();
-  // merge duplicates per row (hash aggregation, emit mode)
+  // merge duplicates per row (hash aggregation, emit mode), two passes: count the distinct
+  // entries of every row, then write them straight into the final CSR (no temporaries)
   Bins B;
   build_bins(c, rptr.p, n, n, B);
-  Buf<int32_t> tk(c.A, rnnz > 0 ? rnnz : 1);
-  Buf<u64> tw(c.A, rnnz > 0 ? rnnz : 1);
   Buf<i64> ocnt(c.A, n);
   Buf<u64> osum(c.A, n);
   LV_CUDA(cudaMemsetAsync(ocnt.p, 0, n * sizeof(i64), c.s));
@@ -236,23 +168,36 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   a.ptr = rptr.p;
   a.keys = rcol.p;
   a.w = rw.p;
-  a.out_key = tk.p;
-  a.out_w = tw.p;
   a.out_cnt = ocnt.p;
   a.out_sum = osum.p;
   // every shared table / hub chunk holds <= 4096 entries of weight <= max w
   const bool narrow = hs[2] < ((u64)1 << 20);
-  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);
-  rcol.release();
-  rw.release();
+  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);  // count pass (out_key == NULL)
   g.row_ptr.alloc(c.A, n + 1);
   exclusive_scan<i64>(c, I64Arr{ocnt.p}, n, g.row_ptr.p, true);
   g.nnz = d2h_i64(c, g.row_ptr.p + n);
+  // weight storage: every merged entry is at most its row sum (<= max δ), so uint32 suffices
+  // whenever max row sum < 2^32, even when W itself is larger (C5)
+  u64 maxrow = 0;
+  {
+    Buf<u64> t(c.A, 1);
+    LV_CUDA(cudaMemsetAsync(t.p, 0, sizeof(u64), c.s));
+    LV_LAUNCH(c, k_max_u64<ArrayIn<u64>>, grid_for(c, n), 256, 0, ArrayIn<u64>{osum.p}, n, t.p);
+    LV_CUDA(cudaMemcpyAsync(&maxrow, t.p, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  }
   if (raw_wt == WT_NONE && g.nnz == rnnz) g.wt = WT_NONE;
-  else g.wt = (g.W < ((i64)1 << 32)) ? WT_U32 : WT_U64;
+  else g.wt = (maxrow < ((u64)1 << 32)) ? WT_U32 : WT_U64;
   g.col.alloc(c.A, g.nnz > 0 ? g.nnz : 1);
   g.w.alloc(c.A, g.nnz * (i64)wbytes(g.wt) + 8);
-  copy_rows(c, g.wt, B, rptr.p, ocnt.p, g.row_ptr.p, tk.p, tw.p, g.col.p, g.w.p);
+  a.out_base = g.row_ptr.p;
+  a.out_key = g.col.p;
+  a.out_w = g.w.p;
+  a.out_w32 = g.wt == WT_U32;
+  a.out_wnone = g.wt == WT_NONE;
+  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);  // write pass
+  rcol.release();
+  rw.release();
   LV_LAUNCH(c, k_delta, grid_for(c, n), 256, 0, n, osum.p, g.loop.p, g.delta.p);
   g.max_delta = max_of(c, g.delta.p, n);
 }
@@ -408,11 +353,9 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   else if (g.wt == WT_U32) permute_t<WU32>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
   else permute_t<WU64>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
   ecnt.release();
-  // aggregate each community's range
+  // aggregate each community's range: count pass, then write straight into the new CSR
   Bins CB;
   build_bins(c, cptr.p, k, k, CB);
-  Buf<int32_t> tk(c.A, tot > 0 ? tot : 1);
-  Buf<u64> tw(c.A, tot > 0 ? tot : 1);
   Buf<i64> ocnt(c.A, k);
   Buf<u64> oself(c.A, k);
   LV_CUDA(cudaMemsetAsync(ocnt.p, 0, k * sizeof(i64), c.s));
@@ -422,24 +365,28 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   a.ptr = cptr.p;
   a.keys = pk.p;
   a.w = pw.p;
-  a.out_key = tk.p;
-  a.out_w = tw.p;
   a.out_cnt = ocnt.p;
   a.out_self = oself.p;
   // a community's row sum is at most its deg_C
   const i64 maxdeg = max_of(c, ndelta.p, k);
-  launch_agg_wt<M_EMIT>(c, g.wt, maxdeg < ((i64)1 << 32), CB, a);
-  pk.release();
-  pw.release();
+  const bool narrow = maxdeg < ((i64)1 << 32);
+  launch_agg_wt<M_EMIT>(c, g.wt, narrow, CB, a);  // count pass (out_key == NULL)
   h.n = k;
   h.W = g.W;
   h.row_ptr.alloc(c.A, k + 1);
   exclusive_scan<i64>(c, I64Arr{ocnt.p}, k, h.row_ptr.p, true);
   h.nnz = d2h_i64(c, h.row_ptr.p + k);
-  h.wt = (g.W < ((i64)1 << 32)) ? WT_U32 : WT_U64;
+  h.wt = narrow ? WT_U32 : WT_U64;  // an entry (c,d) weighs at most deg_C <= maxdeg
   h.col.alloc(c.A, h.nnz > 0 ? h.nnz : 1);
   h.w.alloc(c.A, h.nnz * (i64)wbytes(h.wt) + 8);
-  copy_rows(c, h.wt, CB, cptr.p, ocnt.p, h.row_ptr.p, tk.p, tw.p, h.col.p, h.w.p);
+  a.out_base = h.row_ptr.p;
+  a.out_key = h.col.p;
+  a.out_w = h.w.p;
+  a.out_w32 = h.wt == WT_U32;
+  a.out_wnone = 0;
+  launch_agg_wt<M_EMIT>(c, g.wt, narrow, CB, a);  // write pass
+  pk.release();
+  pw.release();
   h.loop.alloc(c.A, k);
   LV_LAUNCH(c, k_finish_loop, grid_for(c, k), 256, 0, k, nloop.p, oself.p, h.loop.p);
   h.delta = std::move(ndelta);
