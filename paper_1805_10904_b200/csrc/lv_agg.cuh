@@ -740,8 +740,11 @@ struct HubArgs {
   const i64 *bfirst;      // per hub: first fin item (one per bucket)
   const i64 *segoff;      // per chunk: offset of its segment table (nb + 1 entries)
   int32_t *seg;           // segment boundaries, relative to the chunk's pool region
-  int32_t *pkey;          // pool: chunk c owns [c * HUB_CHUNK, (c+1) * HUB_CHUNK)
-  u64 *pval;
+  int32_t *pkey;          // pool: chunk c of this batch owns [(c - c0) * HUB_CHUNK, +HUB_CHUNK)
+  void *pval;             // pool values: uint32 when VT is 32-bit, else u64
+  i64 c0, c1;             // chunk range of this batch (hub rows are processed in batches
+  i64 f0, f1;             //   bounding the pool); fin-item range of the same rows
+  i64 h0, h1;             // hub range of the batch
   const int2 *fitem;      // per fin item: (hub, bucket)
   HubPartial *part;       // per fin item
   u64 *emit_cur;          // per hub (EMIT output cursor)
@@ -810,7 +813,8 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
   if (threadIdx.x == 0) scnt = 0;
   __syncthreads();
-  for (i64 ci = blockIdx.x; ci < hb.nchunks; ci += gridDim.x) {
+  VT *pv = (VT *)hb.pval;
+  for (i64 ci = hb.c0 + blockIdx.x; ci < hb.c1; ci += gridDim.x) {
     const Chunk ch = a.chunks[ci];
     const int32_t r = a.rows[ch.h];
     if (MODE == M_MERGE) {
@@ -830,13 +834,13 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
     for (int b = threadIdx.x; b < nb; b += HUB_ACC_T) seg[b] = hist[b];
     if (threadIdx.x == 0) seg[nb] = n;
     __syncthreads();
-    const i64 base = ci * HUB_CHUNK;
+    const i64 base = (ci - hb.c0) * HUB_CHUNK;
     for (int t = threadIdx.x; t < n; t += HUB_ACC_T) {
       const int sl = slist[t];
       const int32_t k = skeys[sl];
       const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
       hb.pkey[base + pos] = k;
-      hb.pval[base + pos] = (u64)svals[sl];
+      pv[base + pos] = svals[sl];
       skeys[sl] = -1;
       svals[sl] = 0;
     }
@@ -864,7 +868,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
   __syncthreads();
   Grp<HUB_FIN_T, HUB_FIN_T> g;
-  for (i64 fi = blockIdx.x; fi < hb.nfin; fi += gridDim.x) {
+  for (i64 fi = hb.f0 + blockIdx.x; fi < hb.f1; fi += gridDim.x) {
     const int2 it = hb.fitem[fi];
     const int h = it.x, b = it.y;
     const int32_t r = a.rows[h];
@@ -885,7 +889,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         const int32_t *seg = hb.seg + hb.segoff[c];
         const int s0 = seg[b], s1 = seg[b + 1];
         tlen[j] = s1 - s0;
-        tst[j] = c * HUB_CHUNK + s0;
+        tst[j] = (c - hb.c0) * HUB_CHUNK + s0;
       }
       __syncthreads();
       const int total = smem_excl_scan<HUB_FIN_T>(tlen, m);  // tlen[j] = prefix
@@ -898,7 +902,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         }
         const i64 e = tst[lo] + (i - tlen[lo]);
         const int32_t k = hb.pkey[e];
-        const u64 v = hb.pval[e];
+        const u64 v = (u64)((const VT *)hb.pval)[e];
         if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
         bool claimed = false;
         const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, FLG, k, v, &claimed);
@@ -1008,8 +1012,8 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
 template <int MODE>
 __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
   Acc acc;
-  const i64 h = (i64)blockIdx.x * 128 + threadIdx.x;
-  if (h < hb.nhub) {
+  const i64 h = hb.h0 + (i64)blockIdx.x * 128 + threadIdx.x;
+  if (h < hb.h1) {
     const int32_t r = a.rows[h];
     const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
     Cand best;

@@ -78,7 +78,10 @@ struct Bins {
   Buf<Chunk> chunks;
   Buf<i64> cfirst, bfirst, segoff;
   Buf<int32_t> ccount, blg, seg, pkey;
-  Buf<u64> pval, emit_cur;
+  Buf<u64> pval, emit_cur;                 // pval holds uint32 or u64 values (VT)
+  std::vector<i64> batch_h;                // hub-row batches: [batch_h[i], batch_h[i+1])
+  std::vector<i64> h_cfirst, h_bfirst;     // host copies (chunk / fin-item starts, + end)
+  i64 pool_chunks = 0;                     // pool capacity in chunks (max over batches)
   Buf<int2> fitem;
   Buf<HubPartial> part;
   Buf<int> overflow;
@@ -252,8 +255,26 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     B.bfirst.alloc(c.A, B.nhub);
     B.segoff.alloc(c.A, B.nchunks);
     B.seg.alloc(c.A, B.nseg);
-    B.pkey.alloc(c.A, B.nchunks * HUB_CHUNK);
-    B.pval.alloc(c.A, B.nchunks * HUB_CHUNK);
+    // batches of whole hub rows whose chunk pool fits a bound (reused by every batch)
+    // (LV_HUB_POOL_CHUNKS, tests only, forces small batches)
+    static const char *penv = getenv("LV_HUB_POOL_CHUNKS");
+    const i64 POOL_CHUNKS_MAX = penv ? std::max<i64>(1, atoll(penv))
+                                     : std::max<i64>(1, ((i64)4 << 30) / (HUB_CHUNK * 12));  // ~4 GB at u64
+    B.h_cfirst = cfirst;
+    B.h_cfirst.push_back(B.nchunks);
+    B.h_bfirst = bfirst;
+    B.h_bfirst.push_back(B.nfin);
+    B.batch_h.assign(1, 0);
+    B.pool_chunks = 0;
+    for (i64 h = 0; h < B.nhub; ++h) {
+      const i64 hb0 = B.batch_h.back();
+      if (h > hb0 && B.h_cfirst[h + 1] - B.h_cfirst[hb0] > POOL_CHUNKS_MAX) B.batch_h.push_back(h);
+    }
+    B.batch_h.push_back(B.nhub);
+    for (size_t i = 0; i + 1 < B.batch_h.size(); ++i)
+      B.pool_chunks = std::max(B.pool_chunks, B.h_cfirst[B.batch_h[i + 1]] - B.h_cfirst[B.batch_h[i]]);
+    B.pkey.alloc(c.A, B.pool_chunks * HUB_CHUNK);
+    B.pval.alloc(c.A, B.pool_chunks * HUB_CHUNK);  // sized for u64; uint32 uses half
     B.fitem.alloc(c.A, B.nfin);
     B.part.alloc(c.A, B.nfin);
     B.emit_cur.alloc(c.A, B.nhub);
@@ -346,7 +367,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.segoff = B.segoff.p;
     hb.seg = B.seg.p;
     hb.pkey = B.pkey.p;
-    hb.pval = B.pval.p;
+    hb.pval = (void *)B.pval.p;
     hb.fitem = B.fitem.p;
     hb.part = B.part.p;
     hb.emit_cur = B.emit_cur.p;
@@ -367,25 +388,32 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
       LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem));
       attr_fin = fin_smem;
     }
-    if (tm) tm->begin(hub_s, pre + "hub_acc");
     static int occ_acc = -1, occ_fin = -1;
     if (occ_acc < 0) {
       LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_acc, k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem));
-      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_hub_fin<MODE, VT>, HUB_FIN_T,
-                                                            hub_fin_smem<VT>(HUB_FIN_LG)));
+      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_hub_fin<MODE, VT>, HUB_FIN_T, fin_smem));
       occ_acc = std::max(occ_acc, 1);
       occ_fin = std::max(occ_fin, 1);
     }
-    const i64 g_acc = std::min<i64>(B.nchunks, (i64)c.sms * occ_acc);
-    const i64 g_fin = std::min<i64>(B.nfin, (i64)c.sms * occ_fin);
-    LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)g_acc, HUB_ACC_T, acc_smem, a, hb);
-    if (tm) tm->end(hub_s);
-    if (tm) tm->begin(hub_s, pre + "hub_fin");
-    LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
-    if (tm) tm->end(hub_s);
-    if (tm) tm->begin(hub_s, pre + "hub_decide");
-    LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(B.nhub, 128), 128, 0, a, hb);
-    if (tm) tm->end(hub_s);
+    for (size_t bi = 0; bi + 1 < B.batch_h.size(); ++bi) {  // batches of whole hub rows
+      hb.h0 = B.batch_h[bi];
+      hb.h1 = B.batch_h[bi + 1];
+      hb.c0 = B.h_cfirst[hb.h0];
+      hb.c1 = B.h_cfirst[hb.h1];
+      hb.f0 = B.h_bfirst[hb.h0];
+      hb.f1 = B.h_bfirst[hb.h1];
+      const i64 g_acc = std::min<i64>(hb.c1 - hb.c0, (i64)c.sms * occ_acc);
+      const i64 g_fin = std::min<i64>(hb.f1 - hb.f0, (i64)c.sms * occ_fin);
+      if (tm) tm->begin(hub_s, pre + "hub_acc");
+      LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)g_acc, HUB_ACC_T, acc_smem, a, hb);
+      if (tm) tm->end(hub_s);
+      if (tm) tm->begin(hub_s, pre + "hub_fin");
+      LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
+      if (tm) tm->end(hub_s);
+      if (tm) tm->begin(hub_s, pre + "hub_decide");
+      LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(hb.h1 - hb.h0, 128), 128, 0, a, hb);
+      if (tm) tm->end(hub_s);
+    }
   }
   // bins in decreasing length; concurrent mode spreads them over the side streams
   auto st = [&](int k) { return conc ? c.side[(k + 1) % Ctx::NSIDE] : c.s; };

@@ -248,7 +248,8 @@ def test_device_inputs_and_repeat_determinism():
 
 def test_many_hub_buckets_parity():
     """Hub rows split into thousands of hash buckets (the path giant communities take in
-    contraction): a subprocess with a tiny bucket target must match the oracle."""
+    contraction) and processed in many small batches (bounded pool): a subprocess with a
+    tiny bucket target and pool must match the oracle."""
     import subprocess
     import sys
     import os
@@ -267,7 +268,7 @@ def test_many_hub_buckets_parity():
         "        assert g.modularity() == want.final_q\n"
         "print('ok')\n")
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, LV_HUB_BUCKET_TARGET="4",
+    env = dict(os.environ, LV_HUB_BUCKET_TARGET="4", LV_HUB_POOL_CHUNKS="3",
                PYTHONPATH=os.pathsep.join([here, os.path.dirname(here), os.environ.get("PYTHONPATH", "")]))
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
