@@ -67,14 +67,13 @@ struct AggArgs {
   const RowHdr *hdr;       // headers of this bin's rows (smem bins)
   const int32_t *rows;     // rows of this bin
   i64 nrows;
-  const int32_t *keys;     // SWEEP/MERGE: col[] (key = label[col]); EMIT: key directly
+  const int32_t *keys;     // SWEEP/MERGE: col[] (key = packed entry of col); EMIT: key directly
   const void *w;           // weights (WT)
-  const int32_t *label;    // snapshot labels C
+  const u64 *ldeg;         // SWEEP/MERGE: packed snapshot entry per vertex v (see "packed
+                           //   entries" below): lo = C(v) | singlet bit, hi = deg_C(v) (31-bit sat.)
+  const uint32_t *cpk;     // per community c: singlet bit | min(deg_c, 2^31-1)
   int32_t *label_next;     // decisions
-  const i64 *deg;          // deg_C, indexed by label (snapshot)
-  const uint32_t *deg32;   // min(deg_C, 2^32-1): the gathered copy (half the bytes);
-                           // 0xFFFFFFFF means "read deg" (at most one community: Σ deg = 2W)
-  const int32_t *size;     // |C|, indexed by label (snapshot)
+  const i64 *deg;          // deg_C, indexed by label (snapshot; read when the 31-bit copy saturates)
   i64 *deg_next;           // SWEEP/MERGE: copy of deg receiving this pass's moves
   int32_t *size_next;      //   (P:L291 remove/insert; exact int64 atomics, order-free)
   const i64 *delta;        // δ_i
@@ -98,10 +97,28 @@ __device__ __forceinline__ void store_w(const AggArgs &a, i64 o, u64 v) {
   else ((u64 *)a.out_w)[o] = v;
 }
 
-// deg_C through the 32-bit mirror (exact: saturated entries fall back to the 64-bit array)
+// ---- packed entries.  Once per pass every vertex v gets one 8-byte entry
+//   ldeg[v] = { lo: C(v) | (|C(v)| == 1) << 31,  hi: min(deg_C(v), 2^31 - 1) }
+// so the one gather an edge (i, j) makes yields the candidate community, its deg_C (Eq. 2)
+// and its singlet flag — no per-candidate deg/size gathers.  The packed key
+// (label | singlet bit) is what the tables hash: it is a bijection of the label within a
+// pass, so distinct keys are distinct communities.  Labels are < n <= 2^31 - 1, so no
+// packed key equals the empty marker -1 (0xFFFFFFFF).  A saturated deg (2^31 - 1) reads
+// the exact 64-bit deg_C instead (at most 2W / 2^31 communities can saturate).
+constexpr int32_t EMPTY = -1;
+constexpr uint32_t SG_BIT = 0x80000000u;
+constexpr uint32_t DEG_SAT = 0x7FFFFFFFu;
+__device__ __forceinline__ int32_t key_label(int32_t k) { return k & 0x7FFFFFFF; }
+__device__ __forceinline__ int key_sg(int32_t k) { return (int)((uint32_t)k >> 31); }
+__device__ __forceinline__ i64 deg_of(const AggArgs &a, uint32_t d31, int32_t label) {
+  return d31 != DEG_SAT ? (i64)d31 : __ldg(&a.deg[label]);
+}
+// deg_C of community c through the 31-bit copy
 __device__ __forceinline__ i64 load_deg(const AggArgs &a, int32_t c) {
-  const uint32_t d = __ldg(&a.deg32[c]);
-  return d != 0xFFFFFFFFu ? (i64)d : __ldg(&a.deg[c]);
+  return deg_of(a, __ldg(&a.cpk[c]) & DEG_SAT, c);
+}
+__device__ __forceinline__ u64 ld_entry(const AggArgs &a, int32_t v, u64 pol) {
+  return (a.hint & 2) ? (u64)ld_keep((const i64 *)&a.ldeg[v], pol) : __ldg(&a.ldeg[v]);
 }
 
 __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
@@ -111,27 +128,27 @@ __device__ __forceinline__ unsigned hslot(int32_t k, int lg) {
 // Exact 64-bit add (mod 2^64) with native 32-bit atomics: sm_100 has no native 64-bit
 // shared-memory add (it compiles to a CAS loop, which collapses under the same-key
 // contention of later sweeps); the low word's returned old value gives the carry.
-__device__ __forceinline__ void add_u64_split(u64 *p, u64 v) {
-  uint32_t *q = (uint32_t *)p;
+__device__ __forceinline__ void add_u64_split(uint32_t q, u64 v) {
   const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-  const uint32_t old = atomicAdd(q, lo);
+  const uint32_t old = atom_add_s32(q, lo);
   const uint32_t carry = ((uint32_t)(old + lo) < old) ? 1u : 0u;
-  if (hi + carry) atomicAdd(q + 1, hi + carry);
+  if (hi + carry) red_add_s32(q + 4, hi + carry);
 }
 
-// Open-addressing insert with linear probing; keys -1 = empty.  Returns the slot.
-// VT = table value type: uint32_t when the caller has proved every row sum < 2^32
-// (native 32-bit atomics, 9 B per shared slot), else u64.
-template <bool SHARED, class VT>
-__device__ __forceinline__ unsigned tab_insert(int32_t *keys, VT *vals, unsigned mask, int lg, int32_t k, u64 v,
+// Open-addressing insert into a shared-memory table (keys at shared address kb, values
+// at vb) with linear probing; key -1 = empty.  Returns the slot.  VT = table value type:
+// uint32_t when the caller has proved every row sum < 2^32 (native 32-bit atomics), else
+// u64 (split 32-bit atomics).
+template <class VT>
+__device__ __forceinline__ unsigned tab_insert(uint32_t kb, uint32_t vb, unsigned mask, int lg, int32_t k, u64 v,
                                                bool *claimed = nullptr) {
   unsigned h = hslot(k, lg);
   while (true) {
-    int32_t cur = ((volatile int32_t *)keys)[h];
+    const int32_t cur = lds_i32(kb + 4 * h);
     if (cur == k) break;
-    if (cur == -1) {
-      int32_t old = atomicCAS(&keys[h], -1, k);
-      if (old == -1) {
+    if (cur == EMPTY) {
+      const int32_t old = cas_s32(kb + 4 * h, EMPTY, k);
+      if (old == EMPTY) {
         if (claimed) *claimed = true;
         break;
       }
@@ -139,14 +156,18 @@ __device__ __forceinline__ unsigned tab_insert(int32_t *keys, VT *vals, unsigned
     }
     h = (h + 1) & mask;
   }
-  if (sizeof(VT) == 4) atomicAdd((uint32_t *)&vals[h], (uint32_t)v);
-  else if (SHARED) add_u64_split((u64 *)&vals[h], v);
-  else atomicAdd((u64 *)&vals[h], v);
+  if (sizeof(VT) == 4) red_add_s32(vb + 4 * h, (uint32_t)v);
+  else add_u64_split(vb + 8 * h, v);
   return h;
 }
 
-// Exact move score S = 2W·v − δ·deg (Eq. 4 scaled by 2W², reading D4); all four
-// operands are non-negative, so two 64x64->128 unsigned products suffice.
+// ---- exact move scores S = 2W·v − δ·deg (Eq. 4 scaled by 2W², reading D4).  For
+// every candidate of row i, 0 <= v = e_{i->C} <= δ_i and 0 <= deg_C <= 2W (likewise
+// deg_own − δ_i for S_own), so |S| <= 2W·δ_i: rows with 2W·δ_i < 2^63 score in int64
+// (row_s64), the rest in int128 (two 64x64->128 unsigned products).  Both are exact.
+__device__ __forceinline__ bool row_s64(i64 twoW, i64 di) {
+  return __umul64hi((u64)twoW, (u64)di) == 0 && (i64)((u64)twoW * (u64)di) >= 0;
+}
 __device__ __forceinline__ i128 move_score(i64 twoW, u64 v, i64 di, i64 dk) {
   const u128 a = ((u128)__umul64hi((u64)twoW, v) << 64) | (u128)((u64)twoW * v);
   const u128 b = ((u128)__umul64hi((u64)di, (u64)dk) << 64) | (u128)((u64)di * (u64)dk);
@@ -161,23 +182,27 @@ __device__ __forceinline__ int row_lg(i64 d, int lgmax) {
 }
 
 // Insert the row's edges [beg, end) into a table, U edges per lane per batch so the
-// col/w loads and then the label gathers of a batch are independent and in flight
+// col/w loads and then the entry gathers of a batch are independent and in flight
 // together (memory-level parallelism; the atomics would otherwise serialise them).
-template <int G, int U, int MODE, class WT, bool SHARED, bool LIST, class VT>
+// SWEEP/MERGE: the key is the neighbour's packed entry; the thread that claims a slot
+// records the candidate's deg_C next to the slot's list position (odeg[q]).
+template <int G, int U, int MODE, class WT, bool LIST, class VT>
 __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg, i64 end, int32_t *keys, VT *vals,
-                                             unsigned mask, int lg, uint16_t *olist, int *ocnt) {
+                                             unsigned mask, int lg, uint16_t *olist, uint32_t *odeg, int *ocnt) {
   const u64 pf = l2_policy_first(), pl = l2_policy_last();
-  // lane-uniform trip count (every lane of the group runs every batch): required by the
-  // warp-synchronous pre-aggregation below
+  const uint32_t kb = saddr(keys), vb = saddr(vals), cb = saddr(ocnt);
+  // lane-uniform trip count (every lane of the group runs every batch)
   for (i64 b0 = beg; b0 < end; b0 += (i64)G * U) {
     const i64 e0 = b0 + lane;
     int32_t k[U];
+    uint32_t dg[U];
     u64 wv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const i64 e = e0 + (i64)u * G;
-      k[u] = -1;
+      k[u] = EMPTY;
       wv[u] = 0;
+      dg[u] = 0;
       if (e < end) {
         if (a.hint & 1) {
           k[u] = ld_stream(&a.keys[e], pf);
@@ -191,15 +216,23 @@ __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg
     if (MODE != 2 /* M_EMIT */) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (k[u] >= 0) k[u] = (a.hint & 2) ? ld_keep(&a.label[k[u]], pl) : __ldg(&a.label[k[u]]);
+        if (k[u] != EMPTY) {
+          const u64 p = ld_entry(a, k[u], pl);
+          k[u] = (int32_t)(uint32_t)p;
+          dg[u] = (uint32_t)(p >> 32);
+        }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const u64 wsum = wv[u];
-      if (k[u] < 0) continue;
+      if (k[u] == EMPTY) continue;
       bool claimed = false;
-      const unsigned sl = tab_insert<SHARED, VT>(keys, vals, mask, lg, k[u], wsum, LIST ? &claimed : nullptr);
-      if (LIST && claimed) olist[atomicAdd(ocnt, 1)] = (uint16_t)sl;
+      const unsigned sl = tab_insert<VT>(kb, vb, mask, lg, k[u], wsum, LIST ? &claimed : nullptr);
+      if (LIST && claimed) {
+        const int q = (int)atom_add_s32(cb, 1);
+        olist[q] = (uint16_t)sl;
+        if (MODE != 2) odeg[q] = dg[u];
+      }
     }
   }
 }
@@ -222,52 +255,90 @@ struct Grp {
   }
 };
 
-struct Cand {  // lexicographic key (S desc, c asc); c == INT32_MAX means "none"
+// Candidate: lexicographic key (S desc, label asc).  c is the packed key (label | singlet
+// bit, see "packed entries") so the singlet flag travels with it.  "None" has S = -2^127
+// (below every real score, |S| < 2^127) and c = INT32_MAX (no packed key equals it: that
+// would be label 2^31 - 1 >= n).  Rows scored in int64 (row_s64) keep S in lo only.
+struct Cand {
   i64 hi;
   u64 lo;
   int32_t c;
-  int32_t sg;  // |C| == 1 (singlet rule), carried with the candidate
 };
 
+__device__ __forceinline__ Cand cand_none() {
+  Cand x;
+  x.hi = INT64_MIN; x.lo = 0; x.c = INT32_MAX;
+  return x;
+}
+__device__ __forceinline__ Cand cand_none64() {
+  Cand x;
+  x.hi = -1; x.lo = (u64)INT64_MIN; x.c = INT32_MAX;
+  return x;
+}
 __device__ __forceinline__ i128 cand_S(const Cand &x) { return (i128)(((u128)(u64)x.hi << 64) | (u128)x.lo); }
 __device__ __forceinline__ bool cand_better(const Cand &a, const Cand &b) {
-  if (a.c == INT32_MAX) return false;
-  if (b.c == INT32_MAX) return true;
-  i128 sa = cand_S(a), sb = cand_S(b);
-  return sa > sb || (sa == sb && a.c < b.c);
+  const i128 sa = cand_S(a), sb = cand_S(b);
+  return sa > sb || (sa == sb && key_label(a.c) < key_label(b.c));
 }
-__device__ __forceinline__ Cand cand_shfl_xor(const Cand &x, unsigned mask, int o, int width) {
-  Cand y;
-  y.hi = __shfl_xor_sync(mask, x.hi, o, width);
-  y.lo = __shfl_xor_sync(mask, x.lo, o, width);
-  y.c = __shfl_xor_sync(mask, x.c, o, width);
-  return y;
+__device__ __forceinline__ bool cand_better64(const Cand &a, const Cand &b) {
+  const i64 sa = (i64)a.lo, sb = (i64)b.lo;
+  return sa > sb || (sa == sb && key_label(a.c) < key_label(b.c));
 }
 
-// Reduce (best candidate, sum a, sum b, max m) across the group; result valid in the
-// group's lane 0 (thread 0 of the CTA for block groups).
-template <int G, int BLOCK>
-__device__ __forceinline__ void grp_reduce(const Grp<G, BLOCK> &g, Cand &best, u64 &a, u64 &b, int32_t &m) {
+// Argmax of the group's candidates; result valid in the group's lane 0 (thread 0 of the
+// CTA for block groups).  S64: scores are int64 in lo (hi is made its sign extension).
+template <int G, int BLOCK, bool S64>
+__device__ __forceinline__ void grp_argmax(const Grp<G, BLOCK> &g, Cand &best) {
   constexpr int W = G < 32 ? G : 32;
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) {
-    Cand y = cand_shfl_xor(best, g.mask, o, W);
-    if (cand_better(y, best)) best = y;
+    Cand y;
+    y.lo = __shfl_xor_sync(g.mask, best.lo, o, W);
+    y.c = __shfl_xor_sync(g.mask, best.c, o, W);
+    if (S64) {
+      y.hi = 0;
+      if (cand_better64(y, best)) { best.lo = y.lo; best.c = y.c; }
+    } else {
+      y.hi = __shfl_xor_sync(g.mask, best.hi, o, W);
+      if (cand_better(y, best)) best = y;
+    }
+  }
+  if (G > 32) {
+    constexpr int NW = BLOCK / 32;
+    __shared__ Cand sc[NW];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sc[w] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < NW; ++i) {
+        const Cand y = sc[i];
+        if (S64 ? cand_better64(y, best) : cand_better(y, best)) best = y;
+      }
+    }
+    __syncthreads();
+  }
+  if (S64) best.hi = (i64)best.lo >> 63;
+}
+
+// Reduce (sum a, sum b, max m) across the group; result valid in the group's lane 0.
+template <int G, int BLOCK>
+__device__ __forceinline__ void grp_reduce(const Grp<G, BLOCK> &g, u64 &a, u64 &b, int32_t &m) {
+  constexpr int W = G < 32 ? G : 32;
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) {
     a += __shfl_xor_sync(g.mask, a, o, W);
     b += __shfl_xor_sync(g.mask, b, o, W);
     m = max(m, __shfl_xor_sync(g.mask, m, o, W));
   }
   if (G > 32) {
     constexpr int NW = BLOCK / 32;
-    __shared__ Cand sc[NW];
     __shared__ u64 sa[NW], sb[NW];
     __shared__ int32_t sm_[NW];
     const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { sc[w] = best; sa[w] = a; sb[w] = b; sm_[w] = m; }
+    if ((threadIdx.x & 31) == 0) { sa[w] = a; sb[w] = b; sm_[w] = m; }
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int i = 1; i < NW; ++i) {
-        if (cand_better(sc[i], best)) best = sc[i];
         a += sa[i];
         b += sb[i];
         m = max(m, sm_[i]);
@@ -351,102 +422,151 @@ __device__ __forceinline__ void record_move(const AggArgs &a, int32_t own, int32
 // Per-row scalars the group's lane 0 prefetches before the insertion loop (SWEEP).
 struct RowPre {
   i64 dq = 0, dr = 0;  // deg_own, deg_r
-  int32_t szo = 0;     // |own|
 };
+
+// Decision of Algorithm 1 for vertex r from its best candidate: move iff
+// S(best) > S_own (D6), unless both communities are singlets and best's label is larger
+// (singlet rule, D8).  ownk = packed key of r's own community.
+template <bool S64>
+__device__ __forceinline__ void sweep_decide(const AggArgs &a, Acc &acc, int32_t r, int32_t ownk, i64 di, i64 dq,
+                                             i64 dr, const Cand &best, u64 eown) {
+  const int32_t own = key_label(ownk);
+  bool gain;
+  if (S64) {
+    const i64 so = (i64)((u64)a.twoW * eown) - (i64)((u64)di * (u64)(dq - di));
+    gain = (i64)best.lo > so;
+  } else {
+    const i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
+    gain = cand_S(best) > S_own;
+  }
+  int32_t tgt = own;
+  if (best.c != INT32_MAX && gain) {
+    tgt = key_label(best.c);
+    if (key_sg(ownk) && key_sg(best.c) && tgt > own) tgt = own;  // singlet rule (D8)
+  }
+  a.label_next[r] = tgt;
+  if (tgt != own) record_move(a, own, tgt, di);
+  acc.moved += (tgt != own);
+  acc.i2 += eown;
+  acc.add_sq(dr);  // deg of label index r: Σ over all labels gives S2
+}
+
+// Score candidate (packed key k, e_{i->C} = v, deg_C = dk) into best.
+template <bool S64>
+__device__ __forceinline__ void cand_push(Cand &best, i64 twoW, i64 di, int32_t k, u64 v, i64 dk) {
+  if (S64) {
+    const i64 sc = (i64)((u64)twoW * v) - (i64)((u64)di * (u64)dk);
+    const i64 sb = (i64)best.lo;
+    if (sc > sb || (sc == sb && key_label(k) < key_label(best.c))) { best.lo = (u64)sc; best.c = k; }
+  } else {
+    const i128 S = move_score(twoW, v, di, dk);
+    Cand x;
+    x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k;
+    if (cand_better(x, best)) best = x;
+  }
+}
+
+// Isolated-node merge (D14) for a singlet r: cnt distinct neighbouring
+// communities, T the largest label among them, nsg how many of them are singlets.
+__device__ __forceinline__ void merge_decide(const AggArgs &a, Acc &acc, int32_t r, int32_t ownk, u64 cnt, int32_t T,
+                                             u64 nsg) {
+  const int32_t own = key_label(ownk);
+  int32_t tgt = own;
+  if (key_sg(ownk) && cnt == 1) tgt = (nsg && T > own) ? own : T;
+  a.label_next[r] = tgt;
+  if (tgt != own) record_move(a, own, tgt, a.delta[r]);
+  acc.moved += (tgt != own);
+}
 
 // Visits the row's occupied entries — by scanning slots [0,n) (LIST = false) or through
 // the occupied-slot list olist[0..n) (LIST = true) — resets every slot it reads, and
 // applies the mode's epilogue.  Both EMIT passes visit entries in the same order.
+// SWEEP/MERGE: own = packed key of r's community; with LIST, odeg[t] is the deg_C of the
+// entry at list position t (else it is read from cpk).
+// SWEEP epilogue of one row: score every entry, argmax over the group, decide.  The lane
+// that meets r's own community stores e_{i->own} in the group's slot *eown_s (read and
+// cleared by lane 0 after the argmax).
+template <bool S64, int G, int BLOCK, bool LIST, class SlotT, class VT>
+__device__ __forceinline__ void sweep_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, VT *vals, const SlotT *olist,
+                                               const uint32_t *odeg, i64 n, int32_t r, int32_t own, i64 di,
+                                               const RowPre &pre, const AggArgs &a, Acc &acc, u64 *eown_s) {
+  constexpr int U = G < 32 ? 2 : 4;  // entries per lane per batch
+  Cand best = S64 ? cand_none64() : cand_none();
+  u64 ncand = 0;
+  for (i64 t0 = g.lane; t0 < n; t0 += (i64)G * U) {
+    int32_t sl[U], k[U];
+    uint32_t d31[U];
+    u64 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const i64 t = t0 + (i64)u * G;
+      sl[u] = t < n ? (LIST ? (int32_t)olist[t] : (int32_t)t) : -1;
+      d31[u] = (LIST && t < n) ? odeg[t] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      k[u] = sl[u] >= 0 ? keys[sl[u]] : EMPTY;
+      v[u] = 0;
+      if (k[u] != EMPTY) {
+        v[u] = (u64)vals[sl[u]];
+        keys[sl[u]] = EMPTY;
+        vals[sl[u]] = 0;
+        if (!LIST) d31[u] = __ldg(&a.cpk[key_label(k[u])]) & DEG_SAT;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k[u] == EMPTY) continue;
+      if (k[u] == own) {
+        *eown_s = v[u];
+      } else {
+        ++ncand;
+        cand_push<S64>(best, a.twoW, di, k[u], v[u], deg_of(a, d31[u], key_label(k[u])));
+      }
+    }
+  }
+  acc.cand += ncand;
+  grp_argmax<G, BLOCK, S64>(g, best);
+  g.sync();  // *eown_s visible to lane 0
+  if (g.lane == 0) {
+    const u64 eown = *eown_s;
+    *eown_s = 0;
+    sweep_decide<S64>(a, acc, r, own, di, pre.dq, pre.dr, best, eown);
+  }
+}
+
+// Visits the row's occupied entries — by scanning slots [0,n) (LIST = false) or through
+// the occupied-slot list olist[0..n) (LIST = true) — resets every slot it reads, and
+// applies the mode's epilogue.  Both EMIT passes visit entries in the same order.
+// SWEEP/MERGE: own = packed key of r's community; with LIST, odeg[t] is the deg_C of the
+// entry at list position t (else it is read from cpk).
 template <int G, int BLOCK, int MODE, bool LIST, class SlotT, class VT>
 __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, VT *vals, const SlotT *olist,
-                                             i64 n, int32_t r, int32_t own, i64 di, const RowPre &pre,
-                                             const AggArgs &a, Acc &acc) {
-  constexpr int U = G < 32 ? 2 : 4;  // entries per lane per batch: their deg_C gathers overlap
+                                             const uint32_t *odeg, i64 n, int32_t r, int32_t own, i64 di,
+                                             const RowPre &pre, const AggArgs &a, Acc &acc, u64 *eown_s) {
   if (MODE == M_SWEEP) {
-    Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
-    u64 eown = 0, ncand = 0;
-    int32_t dummy = 0;
-    for (i64 t0 = g.lane; t0 < n; t0 += (i64)G * U) {
-      int32_t sl[U], k[U];
-      u64 v[U];
-      i64 dk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const i64 t = t0 + (i64)u * G;
-        sl[u] = t < n ? (LIST ? (int32_t)olist[t] : (int32_t)t) : -1;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        k[u] = sl[u] >= 0 ? keys[sl[u]] : -1;
-        v[u] = 0;
-        if (k[u] >= 0) {
-          v[u] = (u64)vals[sl[u]];
-          keys[sl[u]] = -1;
-          vals[sl[u]] = 0;
-        }
-      }
-#pragma unroll
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        dk[u] = (k[u] >= 0 && k[u] != own) ? load_deg(a, k[u]) : 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (k[u] < 0) continue;
-        if (k[u] == own) {
-          eown = v[u];
-        } else {
-          ++ncand;
-          const i128 S = move_score(a.twoW, v[u], di, dk[u]);
-          Cand x;
-          x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
-          if (cand_better(x, best)) best = x;
-        }
-      }
-    }
-    grp_reduce<G, BLOCK>(g, best, eown, ncand, dummy);
-    if (g.lane == 0) {
-      i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)pre.dq - (i128)di);
-      int32_t tgt = own;
-      if (best.c != INT32_MAX && cand_S(best) > S_own) {
-        tgt = best.c;
-        if (pre.szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule (D8)
-      }
-      a.label_next[r] = tgt;
-      if (tgt != own) record_move(a, own, tgt, di);
-      acc.moved += (tgt != own);
-      acc.i2 += eown;
-      acc.cand += ncand;
-      acc.add_sq(pre.dr);  // deg of label index r: Σ over all labels gives S2
-    }
+    if (row_s64(a.twoW, di)) sweep_epilogue<true, G, BLOCK, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
+    else sweep_epilogue<false, G, BLOCK, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
   } else if (MODE == M_MERGE) {
-    Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
-    u64 cnt = 0, unused = 0;
+    u64 cnt = 0, nsg = 0;
     int32_t T = -1;
     for (i64 t = g.lane; t < n; t += G) {
       const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
       const int32_t k = keys[sl];
-      if (k >= 0) {
-        keys[sl] = -1;
+      if (k != EMPTY) {
+        keys[sl] = EMPTY;
         vals[sl] = 0;
-        if (k != own) { ++cnt; T = max(T, k); }
+        if (k != own) { ++cnt; T = max(T, key_label(k)); nsg += key_sg(k); }
       }
     }
-    grp_reduce<G, BLOCK>(g, none, cnt, unused, T);
-    if (g.lane == 0) {
-      int32_t tgt = own;
-      if (cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
-      a.label_next[r] = tgt;
-      if (tgt != own) record_move(a, own, tgt, a.delta[r]);
-      acc.moved += (tgt != own);
-    }
+    grp_reduce<G, BLOCK>(g, cnt, nsg, T);
+    if (g.lane == 0) merge_decide(a, acc, r, own, cnt, T, nsg);
   } else {  // M_EMIT
     u64 c = 0, selfw = 0, sumw = 0;
     for (i64 t = g.lane; t < n; t += G) {
       const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
       const int32_t k = keys[sl];
-      if (k >= 0) {
+      if (k != EMPTY) {
         const u64 v = (u64)vals[sl];
         sumw += v;
         if (k == r) selfw += v;
@@ -459,9 +579,9 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
     for (i64 t = g.lane; t < n; t += G) {
       const int32_t sl = LIST ? (int32_t)olist[t] : (int32_t)t;
       const int32_t k = keys[sl];
-      if (k >= 0) {
+      if (k != EMPTY) {
         const u64 v = (u64)vals[sl];
-        keys[sl] = -1;
+        keys[sl] = EMPTY;
         vals[sl] = 0;
         if (k != r && a.out_key) {
           a.out_key[o] = k;
@@ -470,10 +590,8 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
         }
       }
     }
-    Cand none;
-    none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
     int32_t dummy = 0;
-    grp_reduce<G, BLOCK>(g, none, selfw, sumw, dummy);
+    grp_reduce<G, BLOCK>(g, selfw, sumw, dummy);
     if (g.lane == 0) {
       a.out_cnt[r] = (i64)tot;
       if (a.out_self) a.out_self[r] = selfw;
@@ -487,15 +605,20 @@ __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *ke
 // epilogue costs O(distinct keys), not O(capacity).
 template <int CAP>
 constexpr bool has_list() { return CAP >= 256; }
-template <int G, int CAP, int BLOCK, class VT>
+// Per group: CAP values, CAP keys, and with a list CAP/2 slot indices (a row of <= CAP/2
+// entries) plus, in SWEEP/MERGE, CAP/2 candidate degrees.
+template <int G, int CAP, int BLOCK, class VT, int MODE>
 constexpr size_t smem_bytes() {
-  return (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(VT) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) + 16);
+  return (size_t)(BLOCK / G) *
+         ((size_t)CAP * (sizeof(VT) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) +
+          ((has_list<CAP>() && MODE != M_EMIT) ? (size_t)CAP * 2 : 0) + 16);
 }
 
 template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   constexpr int GPB = BLOCK / G;
   constexpr bool LIST = has_list<CAP>();
+  constexpr bool DEGL = LIST && MODE != M_EMIT;
   constexpr int LG = (CAP >= 65536) ? 16 : (CAP >= 32768) ? 15 : (CAP >= 16384) ? 14 : (CAP >= 8192) ? 13
                    : (CAP >= 4096) ? 12 : (CAP >= 2048) ? 11 : (CAP >= 1024) ? 10 : (CAP >= 512) ? 9
                    : (CAP >= 256) ? 8 : (CAP >= 128) ? 7 : (CAP >= 64) ? 6 : (CAP >= 32) ? 5
@@ -505,17 +628,21 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   constexpr size_t SB = sizeof(VT) + sizeof(int32_t);
   VT *svals = (VT *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)GPB * CAP * sizeof(VT));
-  uint16_t *slist = (uint16_t *)(sm + (size_t)GPB * CAP * SB);
-  int *scnt = (int *)(sm + (size_t)GPB * CAP * SB + (LIST ? (size_t)GPB * CAP : 0));
+  uint32_t *sdeg = (uint32_t *)(sm + (size_t)GPB * CAP * SB);
+  uint16_t *slist = (uint16_t *)(sm + (size_t)GPB * CAP * SB + (DEGL ? (size_t)GPB * CAP * 2 : 0));
+  // per group 16 B: [0] occupied count (int), [8] e_{i->own} slot (u64)
+  unsigned char *srec = (unsigned char *)slist + (LIST ? (size_t)GPB * CAP : 0);
   Grp<G, BLOCK> g;
   const int grp = threadIdx.x / G;
   int32_t *keys = skeys + grp * CAP;
   VT *vals = svals + grp * CAP;
   uint16_t *olist = slist + grp * (CAP / 2);
-  int *ocnt = scnt + grp;
+  uint32_t *odeg = sdeg + grp * (CAP / 2);
+  int *ocnt = (int *)(srec + 16 * grp);
+  u64 *eown_s = (u64 *)(srec + 16 * grp + 8);
   Acc acc;
-  for (int s = g.lane; s < CAP; s += G) { keys[s] = -1; vals[s] = 0; }
-  if (LIST && g.lane == 0) *ocnt = 0;
+  for (int s = g.lane; s < CAP; s += G) { keys[s] = EMPTY; vals[s] = 0; }
+  if (g.lane == 0) { *ocnt = 0; *eown_s = 0; }
   g.sync();
   const i64 stride = (i64)gridDim.x * GPB;
   i64 idx = (i64)blockIdx.x * GPB + grp;
@@ -527,27 +654,28 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     if (idx + stride < a.nrows) nh = a.hdr[idx + stride];
     const int32_t r = hd.r;
     const i64 beg = hd.beg, end = hd.beg + hd.len;
-    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    u64 pr = 0;  // r's own packed entry
+    if (MODE != M_EMIT) pr = __ldg(&a.ldeg[r]);
+    const int32_t own = (MODE == M_EMIT) ? r : (int32_t)(uint32_t)pr;
     const i64 di = (MODE == M_SWEEP) ? a.delta[r] : 0;
     RowPre pre;
     if (MODE == M_SWEEP && g.lane == 0) {  // issued before the edge loop: overlaps it
-      pre.dq = load_deg(a, own);
+      pre.dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
       pre.dr = load_deg(a, r);
-      pre.szo = __ldg(&a.size[own]);
     }
     if (MODE == M_MERGE) {
-      if (a.size[own] != 1) {
-        if (g.lane == 0) a.label_next[r] = own;
+      if (!key_sg(own)) {
+        if (g.lane == 0) a.label_next[r] = key_label(own);
         continue;
       }
     }
     const int lg = row_lg(end - beg, LG);  // table prefix sized for this row
     const unsigned mask = (1u << lg) - 1u;
-    insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, true, LIST, VT>(a, g.lane, beg, end, keys, vals, mask,
-                                                                                lg, olist, ocnt);
+    insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, LIST, VT>(a, g.lane, beg, end, keys, vals, mask, lg,
+                                                                          olist, odeg, ocnt);
     g.sync();
     const i64 n = LIST ? (i64)(*(volatile int *)ocnt) : ((i64)1 << lg);
-    row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, n, r, own, di, pre, a, acc);
+    row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
     g.sync();
     if (LIST && g.lane == 0) *ocnt = 0;
     g.sync();
@@ -580,24 +708,25 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
     const RowHdr hd = nh;
     if (idx + stride < a.nrows) nh = a.hdr[idx + stride];
     const int32_t r = hd.r;
-    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    u64 pr = 0;  // r's own packed entry
+    if (MODE != M_EMIT) pr = __ldg(&a.ldeg[r]);
+    const int32_t own = (MODE == M_EMIT) ? r : (int32_t)(uint32_t)pr;
     i64 di = 0, dq = 0, dr = 0;
-    int32_t szo = 0;
     if (MODE == M_SWEEP) {
       di = a.delta[r];
       if (g.lane == 0) {
-        dq = load_deg(a, own);
+        dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
         dr = load_deg(a, r);
-        szo = __ldg(&a.size[own]);
       }
     }
     if (MODE == M_MERGE) {
-      if (a.size[own] != 1) {
-        if (g.lane == 0) a.label_next[r] = own;
+      if (!key_sg(own)) {
+        if (g.lane == 0) a.label_next[r] = key_label(own);
         continue;
       }
     }
-    int32_t k = -1;
+    int32_t k = EMPTY;
+    uint32_t d31 = 0;
     u64 w = 0;
     if (g.lane < hd.len) {
       const i64 e = hd.beg + g.lane;
@@ -608,7 +737,11 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
         k = __ldg(&a.keys[e]);
         w = WT::get(a.w, e);
       }
-      if (MODE != M_EMIT) k = __ldg(&a.label[k]);
+      if (MODE != M_EMIT) {
+        const u64 p = __ldg(&a.ldeg[k]);
+        k = (int32_t)(uint32_t)p;
+        d31 = (uint32_t)(p >> 32);
+      }
     }
     bool lead;
     u64 sum;
@@ -626,55 +759,36 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
           if (j < gl) first = false;
         }
       }
-      lead = first && k >= 0;
+      lead = first && k != EMPTY;
     } else {
       const unsigned peers = __match_any_sync(g.mask, k);
-      lead = (__ffs(peers) - 1) == wl && k >= 0;
+      lead = (__ffs(peers) - 1) == wl && k != EMPTY;
       sum = __reduce_add_sync(peers, (uint32_t)w);
     }
     if (MODE == M_SWEEP) {
-      Cand best;
-      best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
-      u64 eown = 0, ncand = 0;
-      int32_t dummy = 0;
-      if (lead) {
-        if (k == own) {
-          eown = sum;
-        } else {
-          ncand = 1;
-          const i64 dk = load_deg(a, k);
-          const i128 S = move_score(a.twoW, sum, di, dk);
-          best.hi = (i64)(S >> 64); best.lo = (u64)S; best.c = k;
-        }
-      }
-      grp_reduce<G, BLOCK>(g, best, eown, ncand, dummy);
-      if (g.lane == 0) {
-        const i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
-        int32_t tgt = own;
-        if (best.c != INT32_MAX && cand_S(best) > S_own) {
-          tgt = best.c;
-          if (szo == 1 && best.c > own && a.size[best.c] == 1) tgt = own;  // singlet rule (D8)
-        }
-        a.label_next[r] = tgt;
-        if (tgt != own) record_move(a, own, tgt, di);
-        acc.moved += (tgt != own);
-        acc.i2 += eown;
-        acc.cand += ncand;
-        acc.add_sq(dr);
+      constexpr int W = G < 32 ? G : 32;
+      const bool cand = lead && k != own;
+      acc.cand += cand;
+      // e_{i->own} from the lane leading r's own community (if any)
+      const unsigned ob = __ballot_sync(g.mask, lead && k == own) & g.mask;
+      const u64 eown = __shfl_sync(g.mask, sum, (__ffs(ob) - 1) & (W - 1), W);
+      if (row_s64(a.twoW, di)) {  // group-uniform
+        Cand best = cand_none64();
+        if (cand) cand_push<true>(best, a.twoW, di, k, sum, deg_of(a, d31, key_label(k)));
+        grp_argmax<G, BLOCK, true>(g, best);
+        if (g.lane == 0) sweep_decide<true>(a, acc, r, own, di, dq, dr, best, ob ? eown : 0);
+      } else {
+        Cand best = cand_none();
+        if (cand) cand_push<false>(best, a.twoW, di, k, sum, deg_of(a, d31, key_label(k)));
+        grp_argmax<G, BLOCK, false>(g, best);
+        if (g.lane == 0) sweep_decide<false>(a, acc, r, own, di, dq, dr, best, ob ? eown : 0);
       }
     } else if (MODE == M_MERGE) {
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
-      u64 cnt = (lead && k != own) ? 1 : 0, unused = 0;
-      int32_t T = (lead && k != own) ? k : -1;
-      grp_reduce<G, BLOCK>(g, none, cnt, unused, T);
-      if (g.lane == 0) {
-        int32_t tgt = own;
-        if (cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
-        a.label_next[r] = tgt;
-        if (tgt != own) record_move(a, own, tgt, a.delta[r]);
-        acc.moved += (tgt != own);
-      }
+      const bool other = lead && k != own;
+      u64 cnt = other ? 1 : 0, nsg = other ? (u64)key_sg(k) : 0;
+      int32_t T = other ? key_label(k) : -1;
+      grp_reduce<G, BLOCK>(g, cnt, nsg, T);
+      if (g.lane == 0) merge_decide(a, acc, r, own, cnt, T, nsg);
     } else {  // M_EMIT: distinct keys != r written compactly at out_base[r]
       const bool emit = lead && k != r;
       const unsigned bal = __ballot_sync(g.mask, emit) & g.mask;
@@ -683,11 +797,9 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
         a.out_key[o] = k;
         store_w(a, o, sum);
       }
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
       u64 selfw = (lead && k == r) ? sum : 0, sumw = lead ? sum : 0;
       int32_t dummy = 0;
-      grp_reduce<G, BLOCK>(g, none, selfw, sumw, dummy);
+      grp_reduce<G, BLOCK>(g, selfw, sumw, dummy);
       if (g.lane == 0) {
         a.out_cnt[r] = (i64)__popc(bal);
         if (a.out_self) a.out_self[r] = selfw;
@@ -742,7 +854,8 @@ struct HubArgs {
   int32_t *seg;           // segment boundaries, relative to the chunk's pool region
   int32_t *pkey;          // pool: chunk c of this batch owns [(c - c0) * HUB_CHUNK, +HUB_CHUNK)
   void *pval;             // pool values: uint32 when VT is 32-bit, else u64
-  i64 c0, c1;             // chunk range of this batch (hub rows are processed in batches
+  uint32_t *pdeg;         // pool: deg_C (31-bit) of each entry (SWEEP/MERGE)
+  i64 c0, c1;            // chunk range of this batch (hub rows are processed in batches
   i64 f0, f1;             //   bounding the pool); fin-item range of the same rows
   i64 h0, h1;             // hub range of the batch
   const int2 *fitem;      // per fin item: (hub, bucket)
@@ -753,15 +866,18 @@ struct HubArgs {
   int fin_lg;             // bucket table log2 capacity of this launch
 };
 
-template <class VT>
+// layouts: [vals | keys | list degrees (SWEEP/MERGE) | list | ...]
+template <class VT, int MODE>
 constexpr size_t hub_acc_smem(int max_blg) {
-  return (size_t)(1 << HUB_SM_LG) * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t) +
+  return (size_t)(1 << HUB_SM_LG) * (sizeof(VT) + sizeof(int32_t)) +
+         (MODE != M_EMIT ? (size_t)HUB_CHUNK * sizeof(uint32_t) : 0) + (size_t)HUB_CHUNK * sizeof(uint16_t) +
          (size_t)((1 << max_blg) + 1) * sizeof(int) + 64;
 }
-template <class VT>
+template <class VT, int MODE>
 constexpr size_t hub_fin_smem(int fin_lg) {
-  return ((size_t)1 << fin_lg) * (sizeof(VT) + sizeof(int32_t)) + ((size_t)1 << (fin_lg - 1)) * sizeof(uint16_t) +
-         (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
+  return ((size_t)1 << fin_lg) * (sizeof(VT) + sizeof(int32_t)) +
+         (MODE != M_EMIT ? ((size_t)1 << (fin_lg - 1)) * sizeof(uint32_t) : 0) +
+         ((size_t)1 << (fin_lg - 1)) * sizeof(uint16_t) + (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
 }
 
 // exclusive scan of cnt[0..n) in shared memory by a CTA of T threads; returns the total
@@ -805,12 +921,14 @@ template <int MODE, class WT, class VT>
 __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   extern __shared__ __align__(16) unsigned char sm[];
   constexpr int CAPS = 1 << HUB_SM_LG;
+  constexpr bool DEGL = MODE != M_EMIT;
   VT *svals = (VT *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)CAPS * sizeof(VT));
-  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)));
-  int *hist = (int *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)) + (size_t)HUB_CHUNK * sizeof(uint16_t));
+  uint32_t *sdeg = (uint32_t *)(sm + (size_t)CAPS * (sizeof(VT) + sizeof(int32_t)));
+  uint16_t *slist = (uint16_t *)((unsigned char *)sdeg + (DEGL ? (size_t)HUB_CHUNK * sizeof(uint32_t) : 0));
+  int *hist = (int *)((unsigned char *)slist + (size_t)HUB_CHUNK * sizeof(uint16_t));
   __shared__ int scnt;
-  for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = -1; svals[s] = 0; }
+  for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = EMPTY; svals[s] = 0; }
   if (threadIdx.x == 0) scnt = 0;
   __syncthreads();
   VT *pv = (VT *)hb.pval;
@@ -818,13 +936,13 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
     const Chunk ch = a.chunks[ci];
     const int32_t r = a.rows[ch.h];
     if (MODE == M_MERGE) {
-      if (a.size[a.label[r]] != 1) continue;  // CTA-uniform
+      if (!key_sg((int32_t)(uint32_t)__ldg(&a.ldeg[r]))) continue;  // CTA-uniform
     }
     const int blg = hb.blg[ch.h];
     const int nb = 1 << blg;
     for (int b = threadIdx.x; b <= nb; b += HUB_ACC_T) hist[b] = 0;
-    insert_range<HUB_ACC_T, 8, MODE, WT, true, true, VT>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1,
-                                                         HUB_SM_LG, slist, &scnt);
+    insert_range<HUB_ACC_T, 8, MODE, WT, true, VT>(a, threadIdx.x, ch.beg, ch.end, skeys, svals, CAPS - 1,
+                                                         HUB_SM_LG, slist, sdeg, &scnt);
     __syncthreads();
     const int n = scnt;
     for (int t = threadIdx.x; t < n; t += HUB_ACC_T) atomicAdd(&hist[hbucket(skeys[slist[t]], blg)], 1);
@@ -841,13 +959,53 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
       const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
       hb.pkey[base + pos] = k;
       pv[base + pos] = svals[sl];
-      skeys[sl] = -1;
+      if (DEGL) hb.pdeg[base + pos] = sdeg[t];
+      skeys[sl] = EMPTY;
       svals[sl] = 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) scnt = 0;
     __syncthreads();
   }
+}
+
+// SWEEP part of one (row, bucket) item: score the bucket's entries (list positions
+// [0, n)), reset their slots, argmax over the CTA (result in thread 0).  The thread that
+// meets r's own community stores e_{i->own} in *eown_s.
+template <bool S64, class VT>
+__device__ __forceinline__ Cand hub_fin_sweep(const Grp<HUB_FIN_T, HUB_FIN_T> &g, int32_t *skeys, VT *svals,
+                                              const uint16_t *slist, const uint32_t *sdeg, int n, int32_t own, i64 di,
+                                              const AggArgs &a, Acc &acc, u64 *eown_s) {
+  constexpr int U = 4;
+  Cand best = S64 ? cand_none64() : cand_none();
+  u64 n1 = 0;
+  for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
+    int32_t sl[U], k[U];
+    uint32_t d31[U];
+    u64 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u * HUB_FIN_T;
+      sl[u] = t < n ? (int32_t)slist[t] : -1;
+      d31[u] = t < n ? sdeg[t] : 0;
+      k[u] = sl[u] >= 0 ? skeys[sl[u]] : EMPTY;
+      v[u] = sl[u] >= 0 ? (u64)svals[sl[u]] : 0;
+      if (sl[u] >= 0) { skeys[sl[u]] = EMPTY; svals[sl[u]] = 0; }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k[u] == EMPTY) continue;
+      if (k[u] == own) {
+        *eown_s = v[u];
+      } else {
+        ++n1;
+        cand_push<S64>(best, a.twoW, di, k[u], v[u], deg_of(a, d31[u], key_label(k[u])));
+      }
+    }
+  }
+  acc.cand += n1;
+  grp_argmax<HUB_FIN_T, HUB_FIN_T, S64>(g, best);  // ends with __syncthreads: *eown_s visible
+  return best;
 }
 
 // Persistent over (row, bucket) items; table reset through the occupied list.
@@ -857,26 +1015,30 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   const int FLG = hb.fin_lg;
   const int CAPF = 1 << FLG;
   const int MAXD = CAPF / 2;
+  constexpr bool DEGL = MODE != M_EMIT;
   VT *svals = (VT *)sm;
   int32_t *skeys = (int32_t *)(sm + (size_t)CAPF * sizeof(VT));
-  uint16_t *slist = (uint16_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
-  i64 *tst = (i64 *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)) + (size_t)MAXD * sizeof(uint16_t));
+  uint32_t *sdeg = (uint32_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
+  uint16_t *slist = (uint16_t *)((unsigned char *)sdeg + (DEGL ? (size_t)MAXD * sizeof(uint32_t) : 0));
+  i64 *tst = (i64 *)((unsigned char *)slist + (size_t)MAXD * sizeof(uint16_t));
   int *tlen = (int *)(tst + HUB_FIN_TILE);
   __shared__ int scnt, sovf;
-  __shared__ u64 sbase;
-  for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = -1; svals[s] = 0; }
-  if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
+  __shared__ u64 sbase, seown;
+  const uint32_t kb = saddr(skeys), vb = saddr(svals);
+  Acc acc;
+  for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = EMPTY; svals[s] = 0; }
+  if (threadIdx.x == 0) { scnt = 0; sovf = 0; seown = 0; }
   __syncthreads();
   Grp<HUB_FIN_T, HUB_FIN_T> g;
   for (i64 fi = hb.f0 + blockIdx.x; fi < hb.f1; fi += gridDim.x) {
     const int2 it = hb.fitem[fi];
     const int h = it.x, b = it.y;
     const int32_t r = a.rows[h];
-    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
+    const int32_t own = (MODE == M_EMIT) ? r : (int32_t)(uint32_t)__ldg(&a.ldeg[r]);
     HubPartial P;
-    P.hi = 0; P.lo = 0; P.c = INT32_MAX; P.T = -1; P.sg = 0; P.pad = 0;
+    P.hi = INT64_MIN; P.lo = 0; P.c = INT32_MAX; P.T = -1; P.sg = 0; P.pad = 0;
     P.eown = 0; P.cnt = 0; P.selfw = 0; P.sumw = 0;
-    if (MODE == M_MERGE && a.size[own] != 1) {  // CTA-uniform
+    if (MODE == M_MERGE && !key_sg(own)) {  // CTA-uniform
       if (threadIdx.x == 0) hb.part[fi] = P;
       continue;
     }
@@ -905,11 +1067,15 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         const u64 v = (u64)((const VT *)hb.pval)[e];
         if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
         bool claimed = false;
-        const unsigned sl = tab_insert<true, VT>(skeys, svals, CAPF - 1, FLG, k, v, &claimed);
+        const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
         if (claimed) {
           const int q = atomicAdd(&scnt, 1);
-          if (q < MAXD) slist[q] = (uint16_t)sl;
-          else sovf = 1;
+          if (q < MAXD) {
+            slist[q] = (uint16_t)sl;
+            if (DEGL) sdeg[q] = hb.pdeg[e];
+          } else {
+            sovf = 1;
+          }
         }
       }
       __syncthreads();
@@ -920,56 +1086,25 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     const int n = min(scnt, MAXD);
     if (MODE == M_SWEEP) {
       const i64 di = a.delta[r];
-      constexpr int U = 4;
       Cand best;
-      best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
-      u64 eown = 0, n1 = 0;
-      int32_t dm = 0;
-      for (int t0 = threadIdx.x; t0 < n; t0 += HUB_FIN_T * U) {
-        int32_t sl[U], k[U];
-        u64 v[U];
-        i64 dk[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int t = t0 + u * HUB_FIN_T;
-          sl[u] = t < n ? (int32_t)slist[t] : -1;
-          k[u] = sl[u] >= 0 ? skeys[sl[u]] : -1;
-          v[u] = sl[u] >= 0 ? (u64)svals[sl[u]] : 0;
-          if (sl[u] >= 0) { skeys[sl[u]] = -1; svals[sl[u]] = 0; }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          dk[u] = (k[u] >= 0 && k[u] != own) ? load_deg(a, k[u]) : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (k[u] < 0) continue;
-          if (k[u] == own) {
-            eown = v[u];
-          } else {
-            ++n1;
-            const i128 S = move_score(a.twoW, v[u], di, dk[u]);
-            Cand x;
-            x.hi = (i64)(S >> 64); x.lo = (u64)S; x.c = k[u];
-            if (cand_better(x, best)) best = x;
-          }
-        }
+      if (row_s64(a.twoW, di)) best = hub_fin_sweep<true, VT>(g, skeys, svals, slist, sdeg, n, own, di, a, acc, &seown);
+      else best = hub_fin_sweep<false, VT>(g, skeys, svals, slist, sdeg, n, own, di, a, acc, &seown);
+      if (threadIdx.x == 0) {
+        P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = seown;
+        seown = 0;
       }
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, best, eown, n1, dm);
-      if (threadIdx.x == 0) { P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.eown = eown; P.cnt = n1; }
     } else if (MODE == M_MERGE) {
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
-      u64 n1 = 0, unused = 0;
+      u64 n1 = 0, nsg = 0;
       int32_t T = -1;
       for (int i = threadIdx.x; i < n; i += HUB_FIN_T) {
         const int sl = slist[i];
         const int32_t k = skeys[sl];
-        skeys[sl] = -1;
+        skeys[sl] = EMPTY;
         svals[sl] = 0;
-        if (k != own) { ++n1; T = max(T, k); }
+        if (k != own) { ++n1; T = max(T, key_label(k)); nsg += key_sg(k); }
       }
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, n1, unused, T);
-      if (threadIdx.x == 0) { P.cnt = n1; P.T = T; }
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, n1, nsg, T);
+      if (threadIdx.x == 0) { P.cnt = n1; P.T = T; P.selfw = nsg; }
     } else {
       u64 n1 = 0, selfw = 0, sumw = 0;
       for (int i = threadIdx.x; i < n; i += HUB_FIN_T) {
@@ -996,10 +1131,8 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         skeys[sl] = -1;
         svals[sl] = 0;
       }
-      Cand none;
-      none.hi = 0; none.lo = 0; none.c = INT32_MAX; none.sg = 0;
       int32_t dm = 0;
-      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, none, selfw, sumw, dm);
+      grp_reduce<HUB_FIN_T, HUB_FIN_T>(g, selfw, sumw, dm);
       if (threadIdx.x == 0) { P.cnt = tot; P.selfw = selfw; P.sumw = sumw; }
     }
     if (threadIdx.x == 0) hb.part[fi] = P;
@@ -1007,6 +1140,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     if (threadIdx.x == 0) { scnt = 0; sovf = 0; }
     __syncthreads();
   }
+  if (MODE == M_SWEEP) acc.flush(a.counters);  // candidate count only
 }
 
 template <int MODE>
@@ -1015,41 +1149,25 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
   const i64 h = hb.h0 + (i64)blockIdx.x * 128 + threadIdx.x;
   if (h < hb.h1) {
     const int32_t r = a.rows[h];
-    const int32_t own = (MODE == M_EMIT) ? r : a.label[r];
-    Cand best;
-    best.hi = 0; best.lo = 0; best.c = INT32_MAX; best.sg = 0;
+    const u64 pr = (MODE == M_EMIT) ? 0 : __ldg(&a.ldeg[r]);
+    const int32_t own = (MODE == M_EMIT) ? r : (int32_t)(uint32_t)pr;
+    Cand best = cand_none();
     u64 eown = 0, cnt = 0, selfw = 0, sumw = 0;
     int32_t T = -1;
     const HubPartial *p = hb.part + hb.bfirst[h];
     const int np = 1 << hb.blg[h];
     for (int j = 0; j < np; ++j) {
       Cand x;
-      x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c; x.sg = p[j].sg;
+      x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
       if (cand_better(x, best)) best = x;
       eown += p[j].eown; cnt += p[j].cnt; selfw += p[j].selfw; sumw += p[j].sumw;
       T = max(T, p[j].T);
     }
     if (MODE == M_SWEEP) {
-      const i64 di = a.delta[r];
-      const i64 dq = load_deg(a, own);
-      i128 S_own = (i128)a.twoW * (i128)(i64)eown - (i128)di * ((i128)dq - (i128)di);
-      int32_t tgt = own;
-      if (best.c != INT32_MAX && cand_S(best) > S_own) {
-        tgt = best.c;
-        if (a.size[own] == 1 && a.size[best.c] == 1 && best.c > own) tgt = own;
-      }
-      a.label_next[r] = tgt;
-      if (tgt != own) record_move(a, own, tgt, di);
-      acc.moved += (tgt != own);
-      acc.i2 += eown;
-      acc.cand += cnt;
-      acc.add_sq(load_deg(a, r));
+      const i64 dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
+      sweep_decide<false>(a, acc, r, own, a.delta[r], dq, load_deg(a, r), best, eown);
     } else if (MODE == M_MERGE) {
-      int32_t tgt = own;
-      if (a.size[own] == 1 && cnt == 1) tgt = (a.size[T] == 1 && T > own) ? own : T;
-      a.label_next[r] = tgt;
-      if (tgt != own) record_move(a, own, tgt, a.delta[r]);
-      acc.moved += (tgt != own);
+      merge_decide(a, acc, r, own, cnt, T, selfw);  // selfw carries the singlet count
     } else {
       a.out_cnt[r] = (i64)cnt;
       if (a.out_self) a.out_self[r] = selfw;
@@ -1077,11 +1195,23 @@ __global__ void __launch_bounds__(256) k_apply_moves(i64 n, const int32_t *__res
   }
 }
 
-// deg32[c] = min(deg[c], 2^32 - 1) (the gathered mirror of deg_C)
-__global__ void __launch_bounds__(256) k_deg32(i64 n, const i64 *__restrict__ deg, uint32_t *deg32) {
+// cpk[c] = (|c| == 1) << 31 | min(deg_c, 2^31 - 1): the per-community half of the packed
+// entries, built once per committed state
+__global__ void __launch_bounds__(256) k_cpk(i64 n, const i64 *__restrict__ deg, const int32_t *__restrict__ size,
+                                             uint32_t *cpk) {
   for (i64 c = (i64)blockIdx.x * 256 + threadIdx.x; c < n; c += (i64)gridDim.x * 256) {
     const i64 d = deg[c];
-    deg32[c] = d >= (i64)0xFFFFFFFF ? 0xFFFFFFFFu : (uint32_t)d;
+    cpk[c] = (size[c] == 1 ? SG_BIT : 0u) | (d >= (i64)DEG_SAT ? DEG_SAT : (uint32_t)d);
+  }
+}
+
+// ldeg[v] = { C(v) | singlet bit, deg_C(v) }: the packed entry every edge gathers
+__global__ void __launch_bounds__(256) k_ldeg(i64 n, const int32_t *__restrict__ label,
+                                              const uint32_t *__restrict__ cpk, u64 *ldeg) {
+  for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256) {
+    const int32_t l = label[v];
+    const uint32_t p = cpk[l];
+    ldeg[v] = ((u64)(p & DEG_SAT) << 32) | (u64)((uint32_t)l | (p & SG_BIT));
   }
 }
 

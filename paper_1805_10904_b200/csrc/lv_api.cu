@@ -223,7 +223,8 @@ namespace {
 struct State {
   Buf<int32_t> lab[2];
   Buf<i64> deg[2];
-  Buf<uint32_t> deg32[2];  // saturating 32-bit mirror of deg (what the kernels gather)
+  Buf<uint32_t> cpk[2];    // singlet bit | min(deg_C, 2^31-1) per community (k_cpk)
+  Buf<u64> ldeg;           // packed entry per vertex, rebuilt from the snapshot each pass (k_ldeg)
   Buf<int32_t> size[2];
   int cur = 0;
 };
@@ -234,9 +235,10 @@ struct SweepOut {
 };
 
 // Algorithmic bytes of one launch of a sweep kernel: per directed edge
-// col 4 + weight wb + neighbour label 4; per distinct candidate deg_C 8; per active
-// vertex 56 (rows[] 4, row_ptr 16, label 4, δ 8, deg_own 8, size_own 4, deg_i 8,
-// label_next 4); commit: 8 B per vertex (two labels) + 56 B per moved vertex.
+// col 4 + weight wb + the neighbour's packed entry 8 (label, singlet bit, deg_C); per
+// active vertex 40 (row header 16, own entry 8, δ 8, deg_i 4, label_next 4).  Per pass:
+// next-state copy 24 B, packing 16 B (label 4 + cpk 4 + entry 8) and the cpk rebuild
+// 16 B (deg 8 + size 4 + cpk 4) per vertex.
 double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<struct SweepOut> &pb,
                         u64 moved);
 
@@ -303,11 +305,12 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   a.ptr = g.row_ptr.p;
   a.keys = g.col.p;
   a.w = g.w.p;
-  a.label = st.lab[st.cur].p;
+  const int32_t *label = st.lab[st.cur].p;
+  const int32_t *size = st.size[st.cur].p;
   a.label_next = st.lab[st.cur ^ 1].p;
   a.deg = st.deg[st.cur].p;
-  a.deg32 = st.deg32[st.cur].p;
-  a.size = st.size[st.cur].p;
+  a.cpk = st.cpk[st.cur].p;
+  a.ldeg = st.ldeg.p;
   i64 *deg_next = st.deg[st.cur ^ 1].p;
   int32_t *size_next = st.size[st.cur ^ 1].p;
   a.deg_next = P.sharded ? nullptr : deg_next;  // sharded: all moves applied after the exchange
@@ -315,7 +318,10 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   if (tm && mode == M_SWEEP) tm->begin(c.s, "sweep_pass");
   if (tm) tm->begin(c.s, "next_state_copy");
   LV_CUDA(cudaMemcpyAsync(deg_next, a.deg, (size_t)g.n * sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
-  LV_CUDA(cudaMemcpyAsync(size_next, a.size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+  LV_CUDA(cudaMemcpyAsync(size_next, size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+  if (tm) tm->end(c.s);
+  if (tm) tm->begin(c.s, "pack_entries");
+  LV_LAUNCH(c, k_ldeg, grid_for(c, g.n), 256, 0, g.n, label, a.cpk, st.ldeg.p);
   if (tm) tm->end(c.s);
   a.delta = g.delta.p;
   a.twoW = 2 * g.W;
@@ -323,8 +329,8 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   if (h->l2mode & 4) {  // keep the snapshot labels resident in the persisting L2 carve-out
     cudaStreamAttrValue v;
     memset(&v, 0, sizeof(v));
-    v.accessPolicyWindow.base_ptr = (void *)st.lab[st.cur].p;
-    v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)g.n * sizeof(int32_t), (size_t)h->l2win);
+    v.accessPolicyWindow.base_ptr = (void *)st.ldeg.p;
+    v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)g.n * sizeof(u64), (size_t)h->l2win);
     v.accessPolicyWindow.hitRatio = 1.0f;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -355,8 +361,8 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
     src = h->dctr.p + SLOT;
   }
   if (P.sharded)  // identical on every rank: apply all moves to the next-state deg/size
-    LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, a.label, a.label_next, g.delta.p, deg_next, size_next);
-  LV_LAUNCH(c, k_deg32, grid_for(c, g.n), 256, 0, g.n, deg_next, st.deg32[st.cur ^ 1].p);
+    LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, label, a.label_next, g.delta.p, deg_next, size_next);
+  LV_LAUNCH(c, k_cpk, grid_for(c, g.n), 256, 0, g.n, deg_next, size_next, st.cpk[st.cur ^ 1].p);
   if (tm && mode == M_SWEEP) tm->end(c.s);
   LV_CUDA(cudaMemcpyAsync(h->hctr, src, (size_t)nsum * SLOT * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
@@ -379,21 +385,20 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   return o;
 }
 
-double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<SweepOut> &pb,
-                        u64 moved) {
+double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<SweepOut> &,
+                        u64) {
   const double wb = wbytes(g.wt);
   for (int b = 0; b < NSMEM; ++b)
-    if (nm == std::string("sweep:") + BIN_NAME[b])
-      return (double)B.edges[b] * (8.0 + wb) + 8.0 * (double)pb[b].cand + 56.0 * (double)B.count(b);
-  if (nm == "sweep:hub_acc") return (double)B.edges[NSMEM] * (8.0 + wb);
-  if (nm == "sweep:hub_fin") return 8.0 * (double)pb[NSMEM].cand;
-  if (nm == "sweep:hub_decide") return 56.0 * (double)B.count(NSMEM);
+    if (nm == std::string("sweep:") + BIN_NAME[b]) return (double)B.edges[b] * (12.0 + wb) + 40.0 * (double)B.count(b);
+  if (nm == "sweep:hub_acc") return (double)B.edges[NSMEM] * (12.0 + wb);
+  if (nm == "sweep:hub_fin") return 0.0;  // pool traffic only: implementation, not algorithm
+  if (nm == "sweep:hub_decide") return 40.0 * (double)B.count(NSMEM);
   if (nm == "next_state_copy") return 24.0 * (double)g.n;  // deg + size: read + write
-  if (nm == "sweep_pass") {  // the whole pass: every bin + hub path + next-state copy
-    double t = 24.0 * (double)g.n;
-    for (int b = 0; b < NSMEM; ++b) t += kernel_alg_bytes(std::string("sweep:") + BIN_NAME[b], B, g, pb, moved);
-    t += kernel_alg_bytes("sweep:hub_acc", B, g, pb, moved) + kernel_alg_bytes("sweep:hub_fin", B, g, pb, moved) +
-         kernel_alg_bytes("sweep:hub_decide", B, g, pb, moved);
+  if (nm == "pack_entries") return 16.0 * (double)g.n;
+  if (nm == "sweep_pass") {  // the whole pass: every bin + hub path + copy + packing + cpk
+    double t = 24.0 * (double)g.n + 16.0 * (double)g.n + 16.0 * (double)g.n;
+    for (int b = 0; b < NSMEM; ++b) t += (double)B.edges[b] * (12.0 + wb) + 40.0 * (double)B.count(b);
+    t += (double)B.edges[NSMEM] * (12.0 + wb) + 40.0 * (double)B.count(NSMEM);
     return t;
   }
   return 0.0;
@@ -417,13 +422,14 @@ void init_state(louvain_ctx *h, const DGraph &g, State &st) {
   for (int b = 0; b < 2; ++b) {
     st.lab[b].alloc(c.A, g.n);
     st.deg[b].alloc(c.A, g.n);
-    st.deg32[b].alloc(c.A, g.n);
+    st.cpk[b].alloc(c.A, g.n);
     st.size[b].alloc(c.A, g.n);
   }
+  st.ldeg.alloc(c.A, g.n);
   st.cur = 0;
   LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg[0].p, st.size[0].p,
             g.delta.p);
-  LV_LAUNCH(c, k_deg32, grid_for(c, g.n), 256, 0, g.n, st.deg[0].p, st.deg32[0].p);
+  LV_LAUNCH(c, k_cpk, grid_for(c, g.n), 256, 0, g.n, st.deg[0].p, st.size[0].p, st.cpk[0].p);
 }
 
 // Level constants: Σ loop and Σ_{inactive} δ² (labels of vertices without neighbours
@@ -808,9 +814,10 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     for (int b = 0; b < 2; ++b) {
       st.lab[b].alloc(c.A, n);
       st.deg[b].alloc(c.A, n);
-      st.deg32[b].alloc(c.A, n);
+      st.cpk[b].alloc(c.A, n);
       st.size[b].alloc(c.A, n);
     }
+    st.ldeg.alloc(c.A, n);
     LV_CUDA(cudaMemcpyAsync(st.lab[0].p, labels_in, n * sizeof(int32_t),
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
     LV_CUDA(cudaMemcpyAsync(st.lab[1].p, st.lab[0].p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
@@ -820,7 +827,7 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
     LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg[0].p, st.size[0].p,
               err.p);
-    LV_LAUNCH(c, k_deg32, grid_for(c, n), 256, 0, n, st.deg[0].p, st.deg32[0].p);
+    LV_LAUNCH(c, k_cpk, grid_for(c, n), 256, 0, n, st.deg[0].p, st.size[0].p, st.cpk[0].p);
     int herr = 0;
     LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));

@@ -79,6 +79,7 @@ struct Bins {
   Buf<i64> cfirst, bfirst, segoff;
   Buf<int32_t> ccount, blg, seg, pkey;
   Buf<u64> pval, emit_cur;                 // pval holds uint32 or u64 values (VT)
+  Buf<uint32_t> pdeg;                      // pool: deg_C of each entry (SWEEP/MERGE)
   std::vector<i64> batch_h;                // hub-row batches: [batch_h[i], batch_h[i+1])
   std::vector<i64> h_cfirst, h_bfirst;     // host copies (chunk / fin-item starts, + end)
   i64 pool_chunks = 0;                     // pool capacity in chunks (max over batches)
@@ -259,7 +260,7 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     // (LV_HUB_POOL_CHUNKS, tests only, forces small batches)
     static const char *penv = getenv("LV_HUB_POOL_CHUNKS");
     const i64 POOL_CHUNKS_MAX = penv ? std::max<i64>(1, atoll(penv))
-                                     : std::max<i64>(1, ((i64)4 << 30) / (HUB_CHUNK * 12));  // ~4 GB at u64
+                                     : std::max<i64>(1, ((i64)4 << 30) / (HUB_CHUNK * 16));  // ~4 GB at u64
     B.h_cfirst = cfirst;
     B.h_cfirst.push_back(B.nchunks);
     B.h_bfirst = bfirst;
@@ -275,6 +276,7 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
       B.pool_chunks = std::max(B.pool_chunks, B.h_cfirst[B.batch_h[i + 1]] - B.h_cfirst[B.batch_h[i]]);
     B.pkey.alloc(c.A, B.pool_chunks * HUB_CHUNK);
     B.pval.alloc(c.A, B.pool_chunks * HUB_CHUNK);  // sized for u64; uint32 uses half
+    B.pdeg.alloc(c.A, B.pool_chunks * HUB_CHUNK);
     B.fitem.alloc(c.A, B.nfin);
     B.part.alloc(c.A, B.nfin);
     B.emit_cur.alloc(c.A, B.nhub);
@@ -316,7 +318,7 @@ template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st) {
   auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT, VT>;
   constexpr int GPB = BLOCK / G;
-  const size_t smem = smem_bytes<G, CAP, BLOCK, VT>();
+  const size_t smem = smem_bytes<G, CAP, BLOCK, VT, MODE>();
   static int occ = -1;
   if (occ < 0) {
     LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -368,6 +370,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.seg = B.seg.p;
     hb.pkey = B.pkey.p;
     hb.pval = (void *)B.pval.p;
+    hb.pdeg = B.pdeg.p;
     hb.fitem = B.fitem.p;
     hb.part = B.part.p;
     hb.emit_cur = B.emit_cur.p;
@@ -376,10 +379,10 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.nchunks = B.nchunks;
     hb.nfin = B.nfin;
     hb.fin_lg = B.fin_lg;
-    const size_t acc_smem = hub_acc_smem<VT>(B.max_blg);
+    const size_t acc_smem = hub_acc_smem<VT, MODE>(B.max_blg);
     static size_t attr_acc = 0;
     static size_t attr_fin = 0;
-    const size_t fin_smem = hub_fin_smem<VT>(B.fin_lg);
+    const size_t fin_smem = hub_fin_smem<VT, MODE>(B.fin_lg);
     if (acc_smem > attr_acc) {
       LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
       attr_acc = acc_smem;

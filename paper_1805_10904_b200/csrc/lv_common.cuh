@@ -214,6 +214,29 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v) {
   return t;
 }
 
+// ---- shared memory through 32-bit shared-window addresses.  Generic-pointer atomics on
+// shared data make the compiler re-derive the CTA's shared window (S2UR SR_CgaCtaId,
+// ULEA, ...) at every access; these take the address once.
+__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int32_t lds_i32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t cas_s32(uint32_t a, int32_t cmp, int32_t val) {
+  int32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(val) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t atom_add_s32(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_s32(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // ---- L2 eviction-priority hints (PTX createpolicy + ld.global.L2::cache_hint).
 // Streams read once (row_ptr, col, w) are marked evict_first so they do not push the
 // randomly gathered arrays (labels, deg_C) out of the 126 MB L2; those are evict_last.
