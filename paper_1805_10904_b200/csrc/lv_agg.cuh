@@ -832,7 +832,6 @@ constexpr int HUB_FIN_LG = 12;
 constexpr int HUB_FIN_LG_MAX = 14;
 constexpr i64 HUB_BUCKET_TARGET = 1024;
 constexpr int HUB_MAX_BLG = 15;    // <= 32768 buckets per row (histogram sized per launch)
-constexpr int HUB_FIN_TILE = 1024; // chunks staged per pass in k_hub_fin
 
 __device__ __forceinline__ unsigned hbucket(int32_t k, int blg) {
   return blg == 0 ? 0u : (((uint32_t)k * 0x85EBCA77u) >> (32 - blg));
@@ -877,7 +876,7 @@ template <class VT, int MODE>
 constexpr size_t hub_fin_smem(int fin_lg) {
   return ((size_t)1 << fin_lg) * (sizeof(VT) + sizeof(int32_t)) +
          (MODE != M_EMIT ? ((size_t)1 << (fin_lg - 1)) * sizeof(uint32_t) : 0) +
-         ((size_t)1 << (fin_lg - 1)) * sizeof(uint16_t) + (size_t)HUB_FIN_TILE * (sizeof(i64) + sizeof(int)) + 64;
+         ((size_t)1 << (fin_lg - 1)) * sizeof(uint16_t) + 64;
 }
 
 // exclusive scan of cnt[0..n) in shared memory by a CTA of T threads; returns the total
@@ -1020,11 +1019,9 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   int32_t *skeys = (int32_t *)(sm + (size_t)CAPF * sizeof(VT));
   uint32_t *sdeg = (uint32_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
   uint16_t *slist = (uint16_t *)((unsigned char *)sdeg + (DEGL ? (size_t)MAXD * sizeof(uint32_t) : 0));
-  i64 *tst = (i64 *)((unsigned char *)slist + (size_t)MAXD * sizeof(uint16_t));
-  int *tlen = (int *)(tst + HUB_FIN_TILE);
   __shared__ int scnt, sovf;
   __shared__ u64 sbase, seown;
-  const uint32_t kb = saddr(skeys), vb = saddr(svals);
+  const uint32_t kb = saddr(skeys), vb = saddr(svals), cb = saddr(&scnt);
   Acc acc;
   for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = EMPTY; svals[s] = 0; }
   if (threadIdx.x == 0) { scnt = 0; sovf = 0; seown = 0; }
@@ -1044,37 +1041,32 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
     }
     const i64 cf = hb.cfirst[h];
     const int nch = hb.ccount[h];
-    for (int t0 = 0; t0 < nch; t0 += HUB_FIN_TILE) {
-      const int m = min(HUB_FIN_TILE, nch - t0);
-      for (int j = threadIdx.x; j < m; j += HUB_FIN_T) {
-        const i64 c = cf + t0 + j;
+    {
+      // every chunk's segment b gets Gc = 256 / nch lanes (a power of two, >= 1): the
+      // segments of an item hold ~2^(fin_lg-2) entries in total, so ~equal work per lane
+      const int per = nch < HUB_FIN_T ? HUB_FIN_T / nch : 1;
+      const int Gc = 1 << (31 - __clz(per));
+      const int ng = HUB_FIN_T / Gc, gid = threadIdx.x / Gc, gl = threadIdx.x % Gc;
+      for (int j = gid; j < nch; j += ng) {
+        const i64 c = cf + j;
         const int32_t *seg = hb.seg + hb.segoff[c];
         const int s0 = seg[b], s1 = seg[b + 1];
-        tlen[j] = s1 - s0;
-        tst[j] = (c - hb.c0) * HUB_CHUNK + s0;
-      }
-      __syncthreads();
-      const int total = smem_excl_scan<HUB_FIN_T>(tlen, m);  // tlen[j] = prefix
-      for (int i = threadIdx.x; i < total; i += HUB_FIN_T) {
-        int lo = 0, hi = m - 1;  // last j with tlen[j] <= i
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (tlen[mid] <= i) lo = mid;
-          else hi = mid - 1;
-        }
-        const i64 e = tst[lo] + (i - tlen[lo]);
-        const int32_t k = hb.pkey[e];
-        const u64 v = (u64)((const VT *)hb.pval)[e];
-        if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
-        bool claimed = false;
-        const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
-        if (claimed) {
-          const int q = atomicAdd(&scnt, 1);
-          if (q < MAXD) {
-            slist[q] = (uint16_t)sl;
-            if (DEGL) sdeg[q] = hb.pdeg[e];
-          } else {
-            sovf = 1;
+        const i64 base = (c - hb.c0) * HUB_CHUNK;
+        for (int i = s0 + gl; i < s1; i += Gc) {
+          const i64 e = base + i;
+          const int32_t k = hb.pkey[e];
+          const u64 v = (u64)((const VT *)hb.pval)[e];
+          if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
+          bool claimed = false;
+          const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
+          if (claimed) {
+            const int q = (int)atom_add_s32(cb, 1);
+            if (q < MAXD) {
+              slist[q] = (uint16_t)sl;
+              if (DEGL) sdeg[q] = hb.pdeg[e];
+            } else {
+              sovf = 1;
+            }
           }
         }
       }
