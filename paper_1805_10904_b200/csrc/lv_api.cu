@@ -90,12 +90,16 @@ double now_ms() {
 }
 
 // ------------------------------------------------------------------ kernels
-__global__ void k_init_state(i64 n, int32_t *l0, int32_t *l1, i64 *deg, int32_t *size, const i64 *delta) {
+// Singleton start: the vertex at position i has label rk[i] (its rank, see compaction +
+// layout; the identity without a layout).
+__global__ void k_init_state(i64 n, int32_t *l0, int32_t *l1, i64 *deg, int32_t *size, const i64 *delta,
+                             const int32_t *rk) {
   for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
-    l0[i] = (int32_t)i;
-    l1[i] = (int32_t)i;
-    deg[i] = delta[i];
-    size[i] = 1;
+    const int32_t l = rk ? rk[i] : (int32_t)i;
+    l0[i] = l;
+    l1[i] = l;
+    deg[l] = delta[i];
+    size[l] = 1;
   }
 }
 
@@ -417,7 +421,7 @@ void account(Prof &P, KTimer &tm, const Bins &B, const DGraph &g, const std::vec
 
 void commit(louvain_ctx *, const DGraph &, State &st, KTimer * = nullptr) { st.cur ^= 1; }
 
-void init_state(louvain_ctx *h, const DGraph &g, State &st) {
+void init_state(louvain_ctx *h, const DGraph &g, State &st, const int32_t *rk = nullptr) {
   Ctx &c = h->c;
   for (int b = 0; b < 2; ++b) {
     st.lab[b].alloc(c.A, g.n);
@@ -428,7 +432,7 @@ void init_state(louvain_ctx *h, const DGraph &g, State &st) {
   st.ldeg.alloc(c.A, g.n);
   st.cur = 0;
   LV_LAUNCH(c, k_init_state, grid_for(c, g.n), 256, 0, g.n, st.lab[0].p, st.lab[1].p, st.deg[0].p, st.size[0].p,
-            g.delta.p);
+            g.delta.p, rk);
   LV_LAUNCH(c, k_cpk, grid_for(c, g.n), 256, 0, g.n, st.deg[0].p, st.size[0].p, st.cpk[0].p);
 }
 
@@ -526,10 +530,10 @@ void run_impl(louvain_ctx *h) {
     // sweep on the order-preserving compaction of g when many vertices are isolated
     DGraph gc;
     Compaction cp;
-    const bool compacted = h->compact && compact_graph(c, *g, 0.9, gc, cp);
+    const bool compacted = h->compact && compact_graph(c, *g, gc, cp);
     const DGraph &gs = compacted ? gc : *g;
     State st;
-    init_state(h, gs, st);
+    init_state(h, gs, st, compacted ? cp.rk.p : nullptr);
     Plan P = make_plan(h, gs);
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t1 = now_ms();
@@ -547,8 +551,8 @@ void run_impl(louvain_ctx *h) {
       lab_o.alloc(c.A, g->n);
       size_o.alloc(c.A, g->n);
       deg_o.alloc(c.A, g->n);
-      LV_LAUNCH(c, k_expand_state, grid_for(c, g->n), 256, 0, g->n, g->row_ptr.p, cp.m.p, cp.inv.p, lab_f, size_f, deg_f,
-                g->delta.p, lab_o.p, size_o.p, deg_o.p);
+      LV_LAUNCH(c, k_expand_state, grid_for(c, g->n), 256, 0, g->n, g->row_ptr.p, cp.m.p, cp.inv.p, cp.pos.p, lab_f,
+                size_f, deg_f, g->delta.p, lab_o.p, size_o.p, deg_o.p);
       lab_f = lab_o.p;
       size_f = size_o.p;
       deg_f = deg_o.p;
@@ -870,13 +874,13 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
     LV_CUDA(cudaSetDevice(c.device));
     DGraph gc;  // sweep what louvain_run sweeps: the compacted level-0 graph when it applies
     Compaction cp;
-    const bool compacted = h->compact && compact_graph(c, h->g0, 0.9, gc, cp);
+    const bool compacted = h->compact && compact_graph(c, h->g0, gc, cp);
     const DGraph &g = compacted ? gc : h->g0;
     Bins Bc;
     if (compacted) build_bins(c, g.row_ptr.p, g.n, g.n, Bc);
     Bins &B = compacted ? Bc : vbins0(h);
     State st;
-    init_state(h, g, st);
+    init_state(h, g, st, compacted ? cp.rk.p : nullptr);
     const Plan PL = plan_of(B);
     for (int i = 0; i < warm; ++i) {
       run_pass(h, g, PL, st, M_SWEEP);

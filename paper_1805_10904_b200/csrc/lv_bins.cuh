@@ -165,8 +165,10 @@ inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
 
 // Partition rows [0,nrows) of `ptr` into length bins; set up hub tables sized for at
 // most `universe` distinct keys per row.
-// Only rows in [lo, hi) are binned (hi < 0: all rows).
-inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B, i64 lo = 0, i64 hi = -1) {
+// Only rows in [lo, hi) are binned (hi < 0: all rows).  rows_only: just B.rows / B.off
+// (the per-bin row lists, ascending within a bin), no headers, edge counts or hub tables.
+inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B, i64 lo = 0, i64 hi = -1,
+                       bool rows_only = false) {
   B.nrows = nrows;
   if (hi < 0) hi = nrows;
   Buf<uint8_t> ids(c.A, nrows > 0 ? nrows : 1);
@@ -186,6 +188,7 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     exclusive_scan<i64>(c, IsBin{ids.p, b}, nrows, pos.p, false);
     LV_LAUNCH(c, k_bin_scatter, grid_for(c, nrows), 256, 0, nrows, ids.p, b, pos.p, B.rows.p + B.off[b]);
   }
+  if (rows_only) return;
   B.hdr.alloc(c.A, B.off[NBIN] > 0 ? B.off[NBIN] : 1);
   if (B.off[NSMEM] > 0)
     LV_LAUNCH(c, k_fill_hdr, grid_for(c, B.off[NSMEM]), 256, 0, B.off[NSMEM], B.rows.p, ptr, B.hdr.p);

@@ -394,45 +394,88 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   LV_CUDA(cudaStreamSynchronize(c.s));
 }
 
-// ------------------------------------------------------------------ compaction
-// Order-preserving removal of vertices without non-loop neighbours from a level graph
-// (they never move and are never gathered).  m[v] = rank of v among the active vertices
-// is monotone, so every label comparison the method makes (min-label ties, the singlet
-// rule, the order-preserving renumbering) is unchanged on the compacted graph, while the
-// gathered label / deg_C arrays shrink to the active vertices (locality in L2).
+// ------------------------------------------------------------------ compaction + layout
+// The graph a level sweeps is a relabelled copy of the level graph g:
+//  * compaction: vertices without non-loop neighbours are removed (they never move and
+//    are never gathered).  rank m[v] of v among the active vertices is monotone, and the
+//    LABEL VALUES of the sweep are these ranks, so every label comparison the method
+//    makes (min-label ties, the singlet rule, the order-preserving renumbering) is the
+//    one it makes on g;
+//  * layout: the vertex POSITIONS (row index, index of every per-vertex array, and of
+//    the edges' neighbour ids) are the ranks ordered by degree bin (ascending rank within
+//    a bin), so each bin's rows, headers and edges are contiguous in HBM (coalesced
+//    streams for the short-row bins) and the high-degree vertices — gathered most often —
+//    share sectors and L2 lines.
+// rk[p] = rank of the vertex at position p (its initial label), pos[i] = position of rank i.
 struct ActiveFlag {
   const i64 *rp;
   __device__ __forceinline__ i64 operator()(i64 v) const { return rp[v + 1] > rp[v] ? 1 : 0; }
 };
 
-__global__ void k_compact_build(i64 n, const i64 *__restrict__ rp, const i64 *__restrict__ delta,
-                                const i64 *__restrict__ loop, const i64 *__restrict__ m, int32_t *inv, i64 *rp_c,
-                                i64 *delta_c, i64 *loop_c) {
+__global__ void k_compact_build(i64 n, const i64 *__restrict__ rp, const i64 *__restrict__ m, int32_t *inv,
+                                i64 *rp_r) {
   for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256) {
     if (rp[v + 1] > rp[v]) {
       const i64 i = m[v];
       inv[i] = (int32_t)v;
-      rp_c[i] = rp[v];
-      delta_c[i] = delta[v];
-      loop_c[i] = loop[v];
+      rp_r[i] = rp[v];  // rank-space row starts (original edge offsets)
     }
   }
 }
 
-__global__ void k_remap_col(i64 nnz, const int32_t *__restrict__ col, const i64 *__restrict__ m, int32_t *col_c) {
-  for (i64 e = (i64)blockIdx.x * 256 + threadIdx.x; e < nnz; e += (i64)gridDim.x * 256) col_c[e] = (int32_t)m[col[e]];
+// per position p: pos[rk[p]] = p, and the position-space row length / δ / loop
+__global__ void k_layout_rows(i64 na, const int32_t *__restrict__ rk, const int32_t *__restrict__ inv,
+                              const i64 *__restrict__ rp, const i64 *__restrict__ delta, const i64 *__restrict__ loop,
+                              int32_t *pos, i64 *len_p, i64 *delta_p, i64 *loop_p) {
+  for (i64 p = (i64)blockIdx.x * 256 + threadIdx.x; p < na; p += (i64)gridDim.x * 256) {
+    const int32_t i = rk[p];
+    const int32_t v = inv[i];
+    pos[i] = (int32_t)p;
+    len_p[p] = rp[v + 1] - rp[v];
+    delta_p[p] = delta[v];
+    loop_p[p] = loop[v];
+  }
 }
 
-// Back to the original index space: labels (compacted community ids -> original vertex
-// ids) and per-community size / deg (indexed by the original label).
+struct LenArr {
+  const i64 *len;
+  __device__ __forceinline__ i64 operator()(i64 p) const { return len[p]; }
+};
+
+// Copy every row of g to its position, neighbour ids mapped to positions (pos[m[col]]).
+// One warp per row (rows of positions [p0, p1)); CTA-per-row for the hub rows.
+template <int T>
+__global__ void __launch_bounds__(T == 32 ? 256 : T) k_layout_edges(i64 p0, i64 p1, const int32_t *__restrict__ rk,
+                                                    const int32_t *__restrict__ inv, const i64 *__restrict__ rp,
+                                                    const int32_t *__restrict__ col, const void *w, int wb,
+                                                    const i64 *__restrict__ m, const int32_t *__restrict__ pos,
+                                                    const i64 *__restrict__ rp_p, int32_t *col_p, void *w_p) {
+  constexpr int G = T == 32 ? 32 : T;  // lanes per row
+  const int per = T == 32 ? (int)(blockDim.x / 32) : 1;
+  const i64 first = (i64)blockIdx.x * per + (T == 32 ? threadIdx.x / 32 : 0);
+  const int lane = threadIdx.x % G;
+  for (i64 p = p0 + first; p < p1; p += (i64)gridDim.x * per) {
+    const int32_t v = inv[rk[p]];
+    const i64 b = rp[v], d = rp[v + 1] - b, o = rp_p[p];
+    for (i64 t = lane; t < d; t += G) {
+      col_p[o + t] = pos[m[col[b + t]]];
+      if (wb == 4) ((uint32_t *)w_p)[o + t] = ((const uint32_t *)w)[b + t];
+      else if (wb == 8) ((u64 *)w_p)[o + t] = ((const u64 *)w)[b + t];
+    }
+  }
+}
+
+// Back to g's index space: labels (rank-valued community ids -> original vertex ids) and
+// per-community size / deg (indexed by the label value = rank).
 __global__ void k_expand_state(i64 n, const i64 *__restrict__ rp, const i64 *__restrict__ m,
-                               const int32_t *__restrict__ inv, const int32_t *__restrict__ lab_c,
-                               const int32_t *__restrict__ size_c, const i64 *__restrict__ deg_c,
-                               const i64 *__restrict__ delta, int32_t *lab_o, int32_t *size_o, i64 *deg_o) {
+                               const int32_t *__restrict__ inv, const int32_t *__restrict__ pos,
+                               const int32_t *__restrict__ lab_c, const int32_t *__restrict__ size_c,
+                               const i64 *__restrict__ deg_c, const i64 *__restrict__ delta, int32_t *lab_o,
+                               int32_t *size_o, i64 *deg_o) {
   for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256) {
     if (rp[v + 1] > rp[v]) {
       const i64 i = m[v];
-      lab_o[v] = inv[lab_c[i]];
+      lab_o[v] = inv[lab_c[pos[i]]];
       size_o[v] = size_c[i];
       deg_o[v] = deg_c[i];
     } else {
@@ -443,23 +486,50 @@ __global__ void k_expand_state(i64 n, const i64 *__restrict__ rp, const i64 *__r
   }
 }
 
+constexpr i64 LONG_ROW = BIN_MAX[NSMEM - 1];  // longer rows take the hub path
+struct LongRow {
+  const i64 *rp;
+  __device__ __forceinline__ i64 operator()(i64 p) const { return rp[p + 1] - rp[p] > LONG_ROW ? 1 : 0; }
+};
+inline i64 count_long_rows(Ctx &c, const DGraph &gc, i64 na) {
+  Buf<u64> t(c.A, 1);
+  LV_CUDA(cudaMemsetAsync(t.p, 0, sizeof(u64), c.s));
+  LV_LAUNCH(c, k_sum_u64<LongRow>, grid_for(c, na), 256, 0, LongRow{gc.row_ptr.p}, na, t.p);
+  u64 h = 0;
+  LV_CUDA(cudaMemcpyAsync(&h, t.p, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  return (i64)h;
+}
+
 struct Compaction {
   i64 na = 0;
-  Buf<i64> m;
-  Buf<int32_t> inv;
+  Buf<i64> m;        // original id -> rank (n + 1; m[n] = na)
+  Buf<int32_t> inv;  // rank -> original id
+  Buf<int32_t> pos;  // rank -> position
+  Buf<int32_t> rk;   // position -> rank
 };
 
-// Builds gc (the compacted level graph) if the active fraction is below `max_frac`.
-inline bool compact_graph(Ctx &c, const DGraph &g, double max_frac, DGraph &gc, Compaction &cp) {
+// Builds gc (the compacted, bin-ordered level graph); false when g has no active vertex.
+inline bool compact_graph(Ctx &c, const DGraph &g, DGraph &gc, Compaction &cp) {
   cp.m.alloc(c.A, g.n + 1);
   exclusive_scan<i64>(c, ActiveFlag{g.row_ptr.p}, g.n, cp.m.p, true);
   cp.na = d2h_i64(c, cp.m.p + g.n);
-  if (cp.na == 0 || (double)cp.na > max_frac * (double)g.n) {
+  if (cp.na == 0) {
     cp.m.release();
     return false;
   }
   const i64 na = cp.na;
   cp.inv.alloc(c.A, na);
+  cp.pos.alloc(c.A, na);
+  cp.rk.alloc(c.A, na);
+  {
+    Buf<i64> rp_r(c.A, na + 1);
+    LV_LAUNCH(c, k_compact_build, grid_for(c, g.n), 256, 0, g.n, g.row_ptr.p, cp.m.p, cp.inv.p, rp_r.p);
+    LV_CUDA(cudaMemcpyAsync(rp_r.p + na, g.row_ptr.p + g.n, sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
+    Bins Br;  // rank-space rows per degree bin
+    build_bins(c, rp_r.p, na, na, Br, 0, -1, true);
+    LV_CUDA(cudaMemcpyAsync(cp.rk.p, Br.rows.p, na * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+  }
   gc.n = na;
   gc.nnz = g.nnz;
   gc.W = g.W;
@@ -468,14 +538,24 @@ inline bool compact_graph(Ctx &c, const DGraph &g, double max_frac, DGraph &gc, 
   gc.row_ptr.alloc(c.A, na + 1);
   gc.delta.alloc(c.A, na);
   gc.loop.alloc(c.A, na);
+  {
+    Buf<i64> len_p(c.A, na);
+    LV_LAUNCH(c, k_layout_rows, grid_for(c, na), 256, 0, na, cp.rk.p, cp.inv.p, g.row_ptr.p, g.delta.p, g.loop.p,
+              cp.pos.p, len_p.p, gc.delta.p, gc.loop.p);
+    exclusive_scan<i64>(c, LenArr{len_p.p}, na, gc.row_ptr.p, true);
+  }
   gc.col.alloc(c.A, g.nnz > 0 ? g.nnz : 1);
   gc.w.alloc(c.A, g.nnz * (i64)wbytes(g.wt) + 8);
-  LV_LAUNCH(c, k_compact_build, grid_for(c, g.n), 256, 0, g.n, g.row_ptr.p, g.delta.p, g.loop.p, cp.m.p, cp.inv.p,
-            gc.row_ptr.p, gc.delta.p, gc.loop.p);
-  LV_CUDA(cudaMemcpyAsync(gc.row_ptr.p + na, g.row_ptr.p + g.n, sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
-  LV_LAUNCH(c, k_remap_col, grid_for(c, g.nnz), 256, 0, g.nnz, g.col.p, cp.m.p, gc.col.p);
-  if (g.wt != WT_NONE)
-    LV_CUDA(cudaMemcpyAsync(gc.w.p, g.w.p, g.nnz * (i64)wbytes(g.wt), cudaMemcpyDeviceToDevice, c.s));
+  // hub rows (> BIN_MAX[NSMEM-1] entries) sit at the end of the layout: a CTA each
+  const i64 nh = count_long_rows(c, gc, na);
+  const i64 ps = na - nh;
+  if (ps > 0)
+    LV_LAUNCH(c, k_layout_edges<32>, grid_for(c, ps, 8), 256, 0, (i64)0, ps, cp.rk.p, cp.inv.p, g.row_ptr.p, g.col.p,
+              (const void *)g.w.p, wbytes(g.wt), cp.m.p, cp.pos.p, gc.row_ptr.p, gc.col.p, (void *)gc.w.p);
+  if (nh > 0)
+    LV_LAUNCH(c, k_layout_edges<512>, (unsigned)std::min<i64>(nh, (i64)c.sms * 4), 512, 0, ps, na, cp.rk.p, cp.inv.p,
+              g.row_ptr.p, g.col.p, (const void *)g.w.p, wbytes(g.wt), cp.m.p, cp.pos.p, gc.row_ptr.p, gc.col.p,
+              (void *)gc.w.p);
   return true;
 }
 
