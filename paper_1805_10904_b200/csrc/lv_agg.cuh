@@ -231,7 +231,7 @@ __device__ __forceinline__ void insert_range(const AggArgs &a, int lane, i64 beg
       if (LIST && claimed) {
         const int q = (int)atom_add_s32(cb, 1);
         olist[q] = (uint16_t)sl;
-        if (MODE != 2) odeg[q] = dg[u];
+        if (MODE != 2 && odeg) odeg[q] = dg[u];
       }
     }
   }
@@ -501,7 +501,7 @@ __device__ __forceinline__ void sweep_epilogue(const Grp<G, BLOCK> &g, int32_t *
     for (int u = 0; u < U; ++u) {
       const i64 t = t0 + (i64)u * G;
       sl[u] = t < n ? (LIST ? (int32_t)olist[t] : (int32_t)t) : -1;
-      d31[u] = (LIST && t < n) ? odeg[t] : 0;
+      d31[u] = (odeg && t < n) ? odeg[t] : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -511,7 +511,7 @@ __device__ __forceinline__ void sweep_epilogue(const Grp<G, BLOCK> &g, int32_t *
         v[u] = (u64)vals[sl[u]];
         keys[sl[u]] = EMPTY;
         vals[sl[u]] = 0;
-        if (!LIST) d31[u] = __ldg(&a.cpk[key_label(k[u])]) & DEG_SAT;
+        if (!odeg) d31[u] = __ldg(&a.cpk[key_label(k[u])]) & DEG_SAT;
       }
     }
 #pragma unroll
@@ -538,8 +538,8 @@ __device__ __forceinline__ void sweep_epilogue(const Grp<G, BLOCK> &g, int32_t *
 // Visits the row's occupied entries — by scanning slots [0,n) (LIST = false) or through
 // the occupied-slot list olist[0..n) (LIST = true) — resets every slot it reads, and
 // applies the mode's epilogue.  Both EMIT passes visit entries in the same order.
-// SWEEP/MERGE: own = packed key of r's community; with LIST, odeg[t] is the deg_C of the
-// entry at list position t (else it is read from cpk).
+// SWEEP/MERGE: own = packed key of r's community; odeg[t] (if not NULL) is the deg_C of
+// the entry at list position t (else it is read from cpk).
 template <int G, int BLOCK, int MODE, bool LIST, class SlotT, class VT>
 __device__ __forceinline__ void row_epilogue(const Grp<G, BLOCK> &g, int32_t *keys, VT *vals, const SlotT *olist,
                                              const uint32_t *odeg, i64 n, int32_t r, int32_t own, i64 di,
@@ -607,18 +607,24 @@ template <int CAP>
 constexpr bool has_list() { return CAP >= 256; }
 // Per group: CAP values, CAP keys, and with a list CAP/2 slot indices (a row of <= CAP/2
 // entries) plus, in SWEEP/MERGE, CAP/2 candidate degrees.
+// (the degree list is dropped — deg_C read from cpk — when it would not fit: u64 tables
+// of the largest bin)
+template <int G, int CAP, int BLOCK, class VT, int MODE>
+constexpr bool has_deg_list() {
+  return has_list<CAP>() && MODE != M_EMIT &&
+         (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(VT) + sizeof(int32_t) + 3) + 16) <= (size_t)220 * 1024;
+}
 template <int G, int CAP, int BLOCK, class VT, int MODE>
 constexpr size_t smem_bytes() {
-  return (size_t)(BLOCK / G) *
-         ((size_t)CAP * (sizeof(VT) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) +
-          ((has_list<CAP>() && MODE != M_EMIT) ? (size_t)CAP * 2 : 0) + 16);
+  return (size_t)(BLOCK / G) * ((size_t)CAP * (sizeof(VT) + sizeof(int32_t)) + (has_list<CAP>() ? CAP : 0) +
+                                (has_deg_list<G, CAP, BLOCK, VT, MODE>() ? (size_t)CAP * 2 : 0) + 16);
 }
 
 template <int G, int CAP, int BLOCK, int MODE, class WT, class VT>
 __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   constexpr int GPB = BLOCK / G;
   constexpr bool LIST = has_list<CAP>();
-  constexpr bool DEGL = LIST && MODE != M_EMIT;
+  constexpr bool DEGL = has_deg_list<G, CAP, BLOCK, VT, MODE>();
   constexpr int LG = (CAP >= 65536) ? 16 : (CAP >= 32768) ? 15 : (CAP >= 16384) ? 14 : (CAP >= 8192) ? 13
                    : (CAP >= 4096) ? 12 : (CAP >= 2048) ? 11 : (CAP >= 1024) ? 10 : (CAP >= 512) ? 9
                    : (CAP >= 256) ? 8 : (CAP >= 128) ? 7 : (CAP >= 64) ? 6 : (CAP >= 32) ? 5
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   int32_t *keys = skeys + grp * CAP;
   VT *vals = svals + grp * CAP;
   uint16_t *olist = slist + grp * (CAP / 2);
-  uint32_t *odeg = sdeg + grp * (CAP / 2);
+  uint32_t *odeg = DEGL ? sdeg + grp * (CAP / 2) : nullptr;
   int *ocnt = (int *)(srec + 16 * grp);
   u64 *eown_s = (u64 *)(srec + 16 * grp + 8);
   Acc acc;

@@ -13,9 +13,9 @@
 namespace lv {
 
 // bin b holds rows of length in (BIN_MAX[b-1], BIN_MAX[b]]; bin NSMEM holds the hubs
-constexpr int NSMEM = 8;
+constexpr int NSMEM = 9;
 constexpr int NBIN = NSMEM + 1;
-constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 4096};
+constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 4096, 8192};
 
 __device__ __forceinline__ int bin_of(i64 d) {
   if (d <= 0) return 255;
@@ -27,7 +27,8 @@ __device__ __forceinline__ int bin_of(i64 d) {
   if (d <= 512) return 5;
   if (d <= 2048) return 6;
   if (d <= 4096) return 7;
-  return 8;
+  if (d <= 8192) return 8;
+  return 9;
 }
 
 struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
@@ -337,9 +338,10 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   if (tm) tm->end(st);
 }
 
-static const char *BIN_NAME[NBIN] = {"reg_g4",         "reg_g8",          "reg_g16",
-                                     "reg_g32",        "agg_g32_c256",    "agg_blk128_c1024",
-                                     "agg_blk256_c4096", "agg_blk512_c8192", "agg_hub"};
+static const char *BIN_NAME[NBIN] = {"reg_g4",           "reg_g8",           "reg_g16",
+                                     "reg_g32",          "agg_g32_c256",     "agg_blk128_c1024",
+                                     "agg_blk256_c4096", "agg_blk512_c8192", "agg_blk1024_c16384",
+                                     "agg_hub"};
 
 // One pass of MODE over every bin of B.  `a` carries the common arguments.  VT is the
 // shared-table value type (uint32_t only when every row sum is known to be < 2^32).
@@ -423,6 +425,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   }
   // bins in decreasing length; concurrent mode spreads them over the side streams
   auto st = [&](int k) { return conc ? c.side[(k + 1) % Ctx::NSIDE] : c.s; };
+  if (B.count(8)) { set(8); launch_bin<1024, 16384, 1024, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[8]).c_str(), st(1)); }
   if (B.count(7)) { set(7); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[7]).c_str(), st(0)); }
   if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str(), st(1)); }
   if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str(), st(2)); }

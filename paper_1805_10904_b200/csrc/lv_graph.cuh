@@ -320,6 +320,7 @@ void permute_t(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, cons
   one(5, k_permute<128, 128, WT>, 1, 128);
   one(6, k_permute<256, 256, WT>, 1, 256);
   one(7, k_permute<256, 256, WT>, 1, 256);
+  one(8, k_permute<256, 256, WT>, 1, 256);
   if (VB.nhub) {
     Buf<i64> hb(c.A, VB.nhub);
     LV_LAUNCH(c, k_hub_bases, grid_for(c, VB.nhub), 256, 0, VB.nhub, VB.rows.p + VB.off[NSMEM], g.row_ptr.p, lab,
