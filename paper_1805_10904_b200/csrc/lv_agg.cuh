@@ -1141,11 +1141,13 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   if (MODE == M_SWEEP) acc.flush(a.counters);  // candidate count only
 }
 
+// One warp per hub row: combine the row's per-bucket partials, then decide / emit.
 template <int MODE>
 __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
   Acc acc;
-  const i64 h = hb.h0 + (i64)blockIdx.x * 128 + threadIdx.x;
-  if (h < hb.h1) {
+  const int lane = threadIdx.x & 31;
+  const i64 h = hb.h0 + (i64)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (h < hb.h1) {  // warp-uniform
     const int32_t r = a.rows[h];
     const u64 pr = (MODE == M_EMIT) ? 0 : __ldg(&a.ldeg[r]);
     const int32_t own = (MODE == M_EMIT) ? r : (int32_t)(uint32_t)pr;
@@ -1154,24 +1156,34 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
     int32_t T = -1;
     const HubPartial *p = hb.part + hb.bfirst[h];
     const int np = 1 << hb.blg[h];
-    for (int j = 0; j < np; ++j) {
+    for (int j = lane; j < np; j += 32) {
       Cand x;
       x.hi = p[j].hi; x.lo = p[j].lo; x.c = p[j].c;
       if (cand_better(x, best)) best = x;
       eown += p[j].eown; cnt += p[j].cnt; selfw += p[j].selfw; sumw += p[j].sumw;
       T = max(T, p[j].T);
     }
-    if (MODE == M_SWEEP) {
-      const i64 dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
-      sweep_decide<false>(a, acc, r, own, a.delta[r], dq, load_deg(a, r), best, eown);
-    } else if (MODE == M_MERGE) {
-      merge_decide(a, acc, r, own, cnt, T, selfw);  // selfw carries the singlet count
-    } else {
-      a.out_cnt[r] = (i64)cnt;
-      if (a.out_self) a.out_self[r] = selfw;
-      if (a.out_sum) a.out_sum[r] = sumw;
+    Grp<32, 128> g;
+    grp_argmax<32, 128, false>(g, best);
+    eown = warp_sum_u64(eown);
+    cnt = warp_sum_u64(cnt);
+    selfw = warp_sum_u64(selfw);
+    sumw = warp_sum_u64(sumw);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) T = max(T, __shfl_xor_sync(0xffffffffu, T, o));
+    if (lane == 0) {
+      if (MODE == M_SWEEP) {
+        const i64 dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
+        sweep_decide<false>(a, acc, r, own, a.delta[r], dq, load_deg(a, r), best, eown);
+      } else if (MODE == M_MERGE) {
+        merge_decide(a, acc, r, own, cnt, T, selfw);  // selfw carries the singlet count
+      } else {
+        a.out_cnt[r] = (i64)cnt;
+        if (a.out_self) a.out_self[r] = selfw;
+        if (a.out_sum) a.out_sum[r] = sumw;
+      }
+      hb.emit_cur[h] = 0;
     }
-    hb.emit_cur[h] = 0;
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }

@@ -605,6 +605,16 @@ void run_impl(louvain_ctx *h) {
   h->ran = true;
 }
 
+// {"<bin name>": [rows, entries], ...} of a level's bins
+std::string bins_json(const Bins &B) {
+  std::string s = "{";
+  for (int b = 0; b < NBIN; ++b) {
+    if (b) s += ", ";
+    s += std::string("\"") + BIN_NAME[b] + "\": [" + std::to_string(B.count(b)) + ", " + std::to_string(B.edges[b]) + "]";
+  }
+  return s + "}";
+}
+
 louvain_status fail(louvain_ctx *h, const Error &e) {
   if (h) h->err = e.msg;
   else g_create_error = e.msg;
@@ -914,7 +924,8 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
                      ", \"alg_bytes_sweep\": " + std::to_string(alg / reps) +
                      ", \"edges\": " + std::to_string(g.nnz) + ", \"n\": " + std::to_string(g.n) +
                      ", \"compacted\": " + (compacted ? std::string("true") : std::string("false")) +
-                     ", \"active\": " + std::to_string(B.active()) + ", \"kernels\": " + P.json(reps) + "}";
+                     ", \"active\": " + std::to_string(B.active()) + ", \"bins\": " + bins_json(B) +
+                     ", \"kernels\": " + P.json(reps) + "}";
     if ((int64_t)js.size() + 1 > cap) return LV_EINVAL;
     memcpy(json, js.c_str(), js.size() + 1);
   } catch (const Error &e) {

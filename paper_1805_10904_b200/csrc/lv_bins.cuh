@@ -419,7 +419,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
       LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
       if (tm) tm->end(hub_s);
       if (tm) tm->begin(hub_s, pre + "hub_decide");
-      LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(hb.h1 - hb.h0, 128), 128, 0, a, hb);
+      LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(hb.h1 - hb.h0, 4), 128, 0, a, hb);
       if (tm) tm->end(hub_s);
     }
   }
