@@ -526,12 +526,33 @@ __device__ __forceinline__ void sweep_epilogue(const Grp<G, BLOCK> &g, int32_t *
     }
   }
   acc.cand += ncand;
-  grp_argmax<G, BLOCK, S64>(g, best);
-  g.sync();  // *eown_s visible to lane 0
-  if (g.lane == 0) {
-    const u64 eown = *eown_s;
-    *eown_s = 0;
-    sweep_decide<S64>(a, acc, r, own, di, pre.dq, pre.dr, best, eown);
+  if (G <= 32) {
+    grp_argmax<G, BLOCK, S64>(g, best);
+    g.sync();  // *eown_s visible to lane 0
+    if (g.lane == 0) {
+      const u64 eown = *eown_s;
+      *eown_s = 0;
+      sweep_decide<S64>(a, acc, r, own, di, pre.dq, pre.dr, best, eown);
+    }
+  } else {
+    // CTA group (the two-barrier row protocol of k_agg_smem): warp argmax, ONE barrier,
+    // thread 0 combines the warps' candidates and decides while the CTA moves on
+    Grp<32, BLOCK> wg;
+    grp_argmax<32, BLOCK, S64>(wg, best);
+    constexpr int NW = BLOCK / 32;
+    __shared__ Cand sc[NW];
+    if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < NW; ++i) {
+        const Cand y = sc[i];
+        if (S64 ? cand_better64(y, best) : cand_better(y, best)) best = y;
+      }
+      if (S64) best.hi = (i64)best.lo >> 63;
+      const u64 eown = *eown_s;
+      *eown_s = 0;
+      sweep_decide<S64>(a, acc, r, own, di, pre.dq, pre.dr, best, eown);
+    }
   }
 }
 
@@ -644,12 +665,17 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
   VT *vals = svals + grp * CAP;
   uint16_t *olist = slist + grp * (CAP / 2);
   uint32_t *odeg = DEGL ? sdeg + grp * (CAP / 2) : nullptr;
-  int *ocnt = (int *)(srec + 16 * grp);
+  int *ocnt2 = (int *)(srec + 16 * grp);  // two occupied counters, alternating per row
   u64 *eown_s = (u64 *)(srec + 16 * grp + 8);
   Acc acc;
   for (int s = g.lane; s < CAP; s += G) { keys[s] = EMPTY; vals[s] = 0; }
-  if (g.lane == 0) { *ocnt = 0; *eown_s = 0; }
+  if (g.lane == 0) { ocnt2[0] = 0; ocnt2[1] = 0; *eown_s = 0; }
   g.sync();
+  // CTA groups sweep a row with two barriers: S1 after the inserts, S2 inside the
+  // epilogue (before thread 0 decides).  Slots are reset by their readers before S2, and
+  // the occupied counter alternates so the next row's is cleared (after S1) without one.
+  constexpr bool TWO_BAR = G > 32 && MODE == M_SWEEP;
+  int par = 0;
   const i64 stride = (i64)gridDim.x * GPB;
   i64 idx = (i64)blockIdx.x * GPB + grp;
   RowHdr nh;  // next row's header, prefetched one iteration ahead
@@ -677,14 +703,21 @@ __global__ void __launch_bounds__(BLOCK) k_agg_smem(AggArgs a) {
     }
     const int lg = row_lg(end - beg, LG);  // table prefix sized for this row
     const unsigned mask = (1u << lg) - 1u;
+    int *ocnt = ocnt2 + par;
     insert_range<G, (G >= 64 ? 8 : (G == 32 ? 4 : 1)), MODE, WT, LIST, VT>(a, g.lane, beg, end, keys, vals, mask, lg,
                                                                           olist, odeg, ocnt);
     g.sync();
     const i64 n = LIST ? (i64)(*(volatile int *)ocnt) : ((i64)1 << lg);
-    row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
-    g.sync();
-    if (LIST && g.lane == 0) *ocnt = 0;
-    g.sync();
+    if (TWO_BAR) {
+      if (g.lane == 0) ocnt2[par ^ 1] = 0;
+      row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
+      par ^= 1;
+    } else {
+      row_epilogue<G, BLOCK, MODE, LIST>(g, keys, vals, olist, odeg, n, r, own, di, pre, a, acc, eown_s);
+      g.sync();
+      if (LIST && g.lane == 0) *ocnt = 0;
+      g.sync();
+    }
   }
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
