@@ -849,6 +849,121 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
 
+// SWEEP over rows of length <= G <= 32, software-pipelined: each group keeps four rows
+// in flight — the header of row i+3, the edge / own-entry / δ loads of row i+2, the
+// entry gather of row i+1 — while it decides row i, so the three dependent global
+// round trips of a short row (header -> col -> ldeg[col]) overlap across rows instead
+// of adding up.  Same arithmetic as k_agg_reg<M_SWEEP>.
+#ifndef LV_REGP_MINB
+#define LV_REGP_MINB 4
+#endif
+struct RegStage {  // per-lane loads of one row (stage B)
+  int32_t col;
+  uint32_t dr31;   // lane 0: cpk[r] (deg_r for S2)
+  u64 w;
+  u64 pr;          // r's own packed entry
+  i64 di;          // δ_r
+};
+
+template <int G, int BLOCK, class WT, bool NARROW>
+__global__ void __launch_bounds__(BLOCK, LV_REGP_MINB) k_sweep_reg(AggArgs a) {
+  constexpr int GPB = BLOCK / G;
+  constexpr int W = G < 32 ? G : 32;
+  Grp<G, BLOCK> g;
+  const int wl = threadIdx.x & 31;
+  Acc acc;
+  const u64 pf = l2_policy_first(), pl = l2_policy_last();
+  const i64 stride = (i64)gridDim.x * GPB;
+  const i64 i0 = (i64)blockIdx.x * GPB + threadIdx.x / G;
+  auto hdr_at = [&](i64 i) {
+    RowHdr h;
+    h.beg = 0; h.r = 0; h.len = 0;
+    if (i < a.nrows) h = a.hdr[i];
+    return h;
+  };
+  auto load_stage = [&](const RowHdr &h, RegStage &E) {
+    E.col = EMPTY; E.w = 0; E.pr = 0; E.di = 0; E.dr31 = 0;
+    if (h.len == 0) return;  // past the end
+    if (g.lane < h.len) {
+      const i64 e = h.beg + g.lane;
+      if (a.hint & 1) {
+        E.col = ld_stream(&a.keys[e], pf);
+        E.w = WT::get(a.w, e, pf);
+      } else {
+        E.col = __ldg(&a.keys[e]);
+        E.w = WT::get(a.w, e);
+      }
+    }
+    E.pr = __ldg(&a.ldeg[h.r]);
+    E.di = __ldg(&a.delta[h.r]);
+    if (g.lane == 0) E.dr31 = __ldg(&a.cpk[h.r]) & DEG_SAT;
+  };
+  RowHdr h0 = hdr_at(i0), h1 = hdr_at(i0 + stride), h2 = hdr_at(i0 + 2 * stride);
+  RegStage E0, E1;
+  load_stage(h0, E0);
+  load_stage(h1, E1);
+  u64 p0 = E0.col != EMPTY ? ld_entry(a, E0.col, pl) : 0;
+  for (i64 i = i0; i < a.nrows; i += stride) {
+    // issue the loads of the rows behind this one
+    const RowHdr h3 = hdr_at(i + 3 * stride);
+    const u64 p1 = E1.col != EMPTY ? ld_entry(a, E1.col, pl) : 0;
+    RegStage E2;
+    load_stage(h2, E2);
+    // decide row i
+    const int32_t r = h0.r;
+    const int32_t own = (int32_t)(uint32_t)E0.pr;
+    const i64 di = E0.di;
+    const int32_t k = E0.col != EMPTY ? (int32_t)(uint32_t)p0 : EMPTY;
+    const uint32_t d31 = (uint32_t)(p0 >> 32);
+    const u64 w = E0.w;
+    bool lead;
+    u64 sum;
+    if (G <= 8 || !NARROW) {  // small groups: an O(G) shuffle scan beats MATCH.ANY
+      sum = 0;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const int32_t kj = __shfl_sync(g.mask, k, j, W);
+        const u64 wj = NARROW ? (u64)__shfl_sync(g.mask, (uint32_t)w, j, W) : __shfl_sync(g.mask, w, j, W);
+        if (kj == k) {
+          sum += wj;
+          if (j < g.lane) first = false;
+        }
+      }
+      lead = first && k != EMPTY;
+    } else {
+      const unsigned peers = __match_any_sync(g.mask, k);
+      lead = (__ffs(peers) - 1) == wl && k != EMPTY;
+      sum = __reduce_add_sync(peers, (uint32_t)w);
+    }
+    const bool cand = lead && k != own;
+    acc.cand += cand;
+    const unsigned ob = __ballot_sync(g.mask, lead && k == own) & g.mask;
+    const u64 eown = __shfl_sync(g.mask, sum, (__ffs(ob) - 1) & (W - 1), W);
+    i64 dq = 0, dr = 0;
+    if (g.lane == 0) {
+      dq = deg_of(a, (uint32_t)(E0.pr >> 32), key_label(own));
+      dr = deg_of(a, E0.dr31, r);
+    }
+    if (row_s64(a.twoW, di)) {  // group-uniform
+      Cand best = cand_none64();
+      if (cand) cand_push<true>(best, a.twoW, di, k, sum, deg_of(a, d31, key_label(k)));
+      grp_argmax<G, BLOCK, true>(g, best);
+      if (g.lane == 0) sweep_decide<true>(a, acc, r, own, di, dq, dr, best, ob ? eown : 0);
+    } else {
+      Cand best = cand_none();
+      if (cand) cand_push<false>(best, a.twoW, di, k, sum, deg_of(a, d31, key_label(k)));
+      grp_argmax<G, BLOCK, false>(g, best);
+      if (g.lane == 0) sweep_decide<false>(a, acc, r, own, di, dq, dr, best, ob ? eown : 0);
+    }
+    // advance the pipeline
+    h0 = h1; h1 = h2; h2 = h3;
+    E0 = E1; E1 = E2;
+    p0 = p1;
+  }
+  acc.flush(a.counters);
+}
+
 // ----------------------------------------------------------------- hub path
 // Rows longer than the largest shared-memory bin (> 4096 entries).  Instead of one
 // global hash table per row (random read-modify-writes over a table far larger than

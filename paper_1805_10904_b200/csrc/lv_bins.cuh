@@ -302,16 +302,22 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
 template <int G, int BLOCK, int MODE, class WT, class VT>
 void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st) {
   constexpr bool NARROW = sizeof(VT) == 4;
-  auto kern = k_agg_reg<G, BLOCK, MODE, WT, NARROW>;
+  // SWEEP rows <= 16: the software-pipelined kernel (measured faster; at G = 32 the plain
+  // one wins).  LV_REG_PIPE=0 / 2 force plain / pipelined everywhere.
+  static const int pipe_env = getenv("LV_REG_PIPE") ? atoi(getenv("LV_REG_PIPE")) : 1;
+  const bool pipe = pipe_env == 2 || (pipe_env == 1 && G <= 16);
+  auto kern = (MODE == M_SWEEP && pipe) ? k_sweep_reg<G, BLOCK, WT, NARROW> : k_agg_reg<G, BLOCK, MODE, WT, NARROW>;
   constexpr int GPB = BLOCK / G;
   static int occ = -1;
   if (occ < 0) {
     int o = 0;
-    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, 0));
+    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, 0));  // (per kernel choice)
     occ = o > 0 ? o : 1;
   }
   i64 grid = cdiv(a.nrows, GPB);
-  i64 cap = (i64)c.sms * occ * 8;
+  // the pipelined kernel at G = 8, 16 is persistent (one resident wave: many rows per
+  // group keep the pipeline full; measured faster), otherwise up to 8 waves
+  i64 cap = (i64)c.sms * occ * ((MODE == M_SWEEP && pipe && G >= 8) ? 1 : 8);
   if (grid > cap) grid = cap;
   if (tm) tm->begin(st, tag);
   LV_LAUNCH_ON(c, st, kern, (unsigned)grid, BLOCK, 0, a);
