@@ -199,7 +199,11 @@ def main():
     dst_h = torch.from_numpy(r.dst).pin_memory()
     w_h = None if r.w is None else torch.from_numpy(r.w).pin_memory()
     out_d = torch.empty(r.n, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream for both legs: the legacy default stream
+    # serialises against torch's allocator traffic (tools/bench_ab.py: +25 % step time)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    torch.cuda.set_stream(stream)
     shard = {}
     if world > 1:  # sweep-sharded (strong scaling): graph replicated, vertex ranges split
         from paper_1805_10904_b200 import dist as lvd
@@ -248,7 +252,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         with Louvain(r.n, src_h.numpy(), dst_h.numpy(), None if w_h is None else w_h.numpy(), device=local,
-                     **shard) as lv:
+                     stream=stream, **shard) as lv:
             lv.run()
             host_out[:] = lv.partition(-1)
     torch.cuda.synchronize()

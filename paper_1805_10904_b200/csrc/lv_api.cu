@@ -11,6 +11,7 @@
 // dropped (never committed) — identical to "commit s, recompute Q, test" of the literal
 // algorithm, without a separate edge pass per sweep.
 #include <cuda_runtime.h>
+#include <cuda_profiler_api.h>
 #include <dlfcn.h>
 
 #include <chrono>
@@ -897,6 +898,9 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
       commit(h, g, st);
     }
     LV_CUDA(cudaStreamSynchronize(c.s));
+    // LV_PROFILE_RANGE=1: bracket the timed passes for `ncu --profile-from-start off`
+    const bool prange = getenv("LV_PROFILE_RANGE") != nullptr;
+    if (prange) cudaProfilerStart();
     KTimer tm;
     tm.on = true;
     Prof P;
@@ -916,6 +920,7 @@ louvain_status louvain_time_sweeps(louvain_t h, int32_t warm, int32_t reps, char
       total_ms += ms;
       account(P, tm, B, g, pb, o.moved);
     }
+    if (prange) cudaProfilerStop();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     double alg = 0;
