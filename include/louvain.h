@@ -54,7 +54,9 @@ typedef enum {
 typedef enum {
     LV_W_NONE = 0, /* unweighted: every weight is 1 (reading D1; P:L43 says "0")        */
     LV_W_I32 = 1,  /* int32 weights, each > 0                                           */
-    LV_W_I64 = 2   /* int64 weights, each > 0                                           */
+    LV_W_I64 = 2,  /* int64 weights, each > 0                                           */
+    LV_W_F32 = 3,  /* real weights (P:L247 stores floats), each finite and > 0; mapped to  */
+    LV_W_F64 = 4   /* fixed point w~ = rint(w * 2^s), s max with sum w~ <= 2^52 (D28)       */
 } louvain_wtype;
 
 /* Undirected graph G(V,E,ω) as COO records, each undirected edge once; loops
@@ -106,6 +108,13 @@ louvain_status louvain_create(const louvain_graph *g, const louvain_config *cfg,
 
 /* Run Algorithm 2 to completion (blocking).  May be called again to re-run. */
 louvain_status louvain_run(louvain_t h);
+
+/* Fixed-point scale s of a real-weighted graph (LV_W_F32/F64; reading D28, SURVEY §8(f)
+ * F1): the library runs on w~ = rint(w * 2^s), the largest s with sum w~ <= 2^52, so
+ * every sum and score stays exact; Q is that of the fixed-point graph (within m * 2^-s
+ * relative of the real-weight Q).  0 for integer inputs.  Errors: LV_EINVAL.  (Create
+ * fails with LV_EGRAPH if a real weight is not finite and > 0, or rounds to 0 at s.) */
+louvain_status louvain_weight_scale(louvain_t h, int32_t *s);
 
 /* Number of recorded dendrogram levels (>= 1 after run). */
 louvain_status louvain_num_levels(louvain_t h, int32_t *levels);

@@ -30,7 +30,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
     ):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -73,6 +73,10 @@ def _L():
         GP = C.POINTER(_Graph)
         lib.og_graph_build.argtypes = [i64, i64, P, P, P, C.POINTER(GP)]
         lib.og_graph_build.restype = C.c_int
+        lib.og_graph_build_real.argtypes = [i64, i64, P, P, P, C.POINTER(i32), C.POINTER(GP)]
+        lib.og_graph_build_real.restype = C.c_int
+        lib.og_fixed_sum.argtypes = [i64, P, i32]
+        lib.og_fixed_sum.restype = i64
         lib.og_graph_free.argtypes = [GP]
         lib.og_modularity.argtypes = [GP, P, P, P, P, P]
         lib.og_modularity.restype = C.c_int
@@ -128,15 +132,25 @@ class Graph:
 
     @classmethod
     def from_edges(cls, n, src, dst, w=None) -> "Graph":
+        """Integer weights (or None = 1) build directly; float weights go through the
+        fixed-point mapping of reading D28 (``og_graph_build_real``; ``g.scale`` = s)."""
         src = np.ascontiguousarray(src, dtype=np.int32)
         dst = np.ascontiguousarray(dst, dtype=np.int32)
-        wa = None if w is None else np.ascontiguousarray(w, dtype=np.int64)
         h = C.POINTER(_Graph)()
-        rc = _L().og_graph_build(int(n), len(src), _ptr(src), _ptr(dst), _ptr(wa), C.byref(h))
+        scale = None
+        if w is not None and np.asarray(w).dtype.kind == "f":
+            wa = np.ascontiguousarray(w, dtype=np.float64)
+            s = C.c_int32()
+            rc = _L().og_graph_build_real(int(n), len(src), _ptr(src), _ptr(dst), _ptr(wa), C.byref(s), C.byref(h))
+            scale = s.value
+        else:
+            wa = None if w is None else np.ascontiguousarray(w, dtype=np.int64)
+            rc = _L().og_graph_build(int(n), len(src), _ptr(src), _ptr(dst), _ptr(wa), C.byref(h))
         if rc not in (0, 3) or not h:
             raise OracleError(f"og_graph_build failed rc={rc}")
         g = cls(h)
         g.rc = rc
+        g.scale = scale
         return g
 
     def __del__(self):
@@ -198,6 +212,12 @@ class Graph:
         if rc:
             raise OracleError(f"og_induce rc={rc}")
         return Graph(h)
+
+
+def fixed_sum(w, s: int) -> int:
+    """T(s) = Σ rint(ω·2^s), saturated at 2^62 (reading D28)."""
+    wa = np.ascontiguousarray(w, dtype=np.float64)
+    return int(_L().og_fixed_sum(len(wa), _ptr(wa), int(s)))
 
 
 def renumber(labels):

@@ -127,6 +127,53 @@ int og_graph_build(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
     return W > 0 ? OG_OK : OG_EZEROW;
 }
 
+/* ------------------------------------------------ real weights (F1, reading D28) */
+
+/* rint(ω · 2^s): ldexp is exact whenever the result is >= 2^-1022 (a power-of-two
+ * scaling), and anything smaller rounds to 0 either way; rint rounds half to even in
+ * the default rounding mode. */
+static double fixed_of(double w, int32_t s) { return rint(ldexp(w, s)); }
+
+int64_t og_fixed_sum(int64_t m, const double *w, int32_t s) {
+    const double cap = 4611686018427387904.0;   /* 2^62 */
+    __int128 t = 0;
+    for (int64_t k = 0; k < m; ++k) {
+        double x = fixed_of(w[k], s);
+        if (!(x < cap)) return (int64_t)cap;      /* also catches inf */
+        t += (__int128)(int64_t)x;
+        if (t >= (__int128)(int64_t)cap) return (int64_t)cap;
+    }
+    return (int64_t)t;
+}
+
+int og_graph_build_real(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                        const double *w, int32_t *s_out, og_graph **out) {
+    *out = NULL;
+    if (n <= 0 || m < 0 || !w || !s_out) return OG_EINVAL;
+    for (int64_t k = 0; k < m; ++k)
+        if (!(w[k] > 0.0) || !isfinite(w[k])) return OG_EGRAPH;      /* P:L43 positive */
+    const int64_t lim = (int64_t)1 << 52;
+    /* T(s) is non-decreasing in s: binary search the largest s with T(s) <= 2^52 over
+     * [-1100, 1100] (T(-1100) = 0; T(1100) saturates for any ω > 0 when m > 0). */
+    int32_t lo = -1100, hi = 1100;              /* invariant: T(lo) <= lim < T(hi) */
+    if (m == 0) hi = lo;                        /* W = 0 below anyway */
+    while (hi - lo > 1) {
+        int32_t mid = lo + (hi - lo) / 2;
+        if (og_fixed_sum(m, w, mid) <= lim) lo = mid; else hi = mid;
+    }
+    const int32_t s = lo;
+    int64_t *wi = (int64_t *)malloc((size_t)(m > 0 ? m : 1) * sizeof(int64_t));
+    if (!wi) return OG_ENOMEM;
+    for (int64_t k = 0; k < m; ++k) {
+        wi[k] = (int64_t)fixed_of(w[k], s);
+        if (wi[k] <= 0) { free(wi); return OG_EGRAPH; }   /* ω~ = 0: range beyond 52 bits */
+    }
+    *s_out = s;
+    int rc = og_graph_build(n, m, src, dst, wi, out);
+    free(wi);
+    return rc;
+}
+
 /* ----------------------------------------------------------- community state */
 
 struct og_state {

@@ -62,6 +62,20 @@ int  og_graph_build(int64_t n, int64_t m, const int32_t *src, const int32_t *dst
                     const int64_t *w, og_graph **out);
 void og_graph_free(og_graph *g);
 
+/* SURVEY §8(f) F1, reading D28: real weights ω (the paper stores float
+ * weights; any finite ω > 0, given here as binary64 — binary32 inputs convert
+ * exactly) are mapped to the fixed-point integers
+ *     ω~_k = rint(ω_k · 2^s)     (round half to even; ω·2^s is exact in binary64)
+ * with s the LARGEST integer such that Σ_k ω~_k <= 2^52 (so W~ <= 2^52 and every
+ * aggregate is an exact integer, also exactly representable in fp64).  The graph of the
+ * ω~ then runs the integer method unchanged.  Returns OG_EGRAPH if an ω is not finite or
+ * <= 0, or if some ω~_k = 0 at that s (dynamic range beyond 52 bits); *s_out = s. */
+int  og_graph_build_real(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                         const double *w, int32_t *s_out, og_graph **out);
+/* T(s) = Σ_k rint(ω_k · 2^s) as an exact integer, saturated at 2^62 (helper of the above;
+ * exported for the pins). */
+int64_t og_fixed_sum(int64_t m, const double *w, int32_t s);
+
 /* Eq. 3 on partition `labels` (any int32 labels in [0,n)).  Outputs the exact
  * numerators I2 = Σ_i e_{i→C(i)} + 2Σloop, S2 = Σ_C deg_C² (as hi/lo words) and
  * Q = d(2W·I2 − S2) / d(4W²) (D22, D24). */

@@ -203,6 +203,7 @@ struct louvain_ctx {
   bool shard = false;
   int world = 1, rank = 0, sim = 0;
   void *comm = nullptr;
+  int32_t wscale = 0;          // s of the real-weight fixed point (D28); 0 for integer input
   bool compact = true;         // LV_NO_COMPACT=1 disables the per-level compaction
   int l2mode = 1;              // LV_L2MODE: bit0 evict_first streams (default), bit1 evict_last
                                // gathers, bit2 persisting L2 window on the snapshot labels
@@ -654,7 +655,7 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
   *out = nullptr;
   g_create_error.clear();
   if (!gr || gr->n <= 0 || gr->m < 0 || (gr->m > 0 && (!gr->src || !gr->dst)) ||
-      (gr->wtype != LV_W_NONE && gr->m > 0 && !gr->w) || gr->wtype < 0 || gr->wtype > 2 || gr->n > 0x7fffffffLL) {
+      (gr->wtype != LV_W_NONE && gr->m > 0 && !gr->w) || gr->wtype < 0 || gr->wtype > 4 || gr->n > 0x7fffffffLL) {
     g_create_error = "invalid graph arguments";
     return LV_EINVAL;
   }
@@ -731,13 +732,20 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       src = dsrc.p;
       dst = ddst.p;
       if (gr->wtype != LV_W_NONE) {
-        const size_t wb = gr->wtype == LV_W_I32 ? 4 : 8;
+        const size_t wb = (gr->wtype == LV_W_I32 || gr->wtype == LV_W_F32) ? 4 : 8;
         dw.alloc(h->c.A, gr->m * wb);
         LV_CUDA(cudaMemcpyAsync(dw.p, gr->w, gr->m * wb, cudaMemcpyHostToDevice, h->c.s));
         w = dw.p;
       }
     }
-    build_csr(h->c, gr->n, gr->m, src, dst, w, gr->wtype, h->g0);
+    int wtype = gr->wtype;
+    Buf<i64> wq;
+    if (wtype == LV_W_F32 || wtype == LV_W_F64) {  // real weights -> fixed point (F1, D28)
+      h->wscale = quantize_real(h->c, gr->m, w, wtype, wq);
+      w = wq.p;
+      wtype = LV_W_I64;
+    }
+    build_csr(h->c, gr->n, gr->m, src, dst, w, wtype, h->g0);
     h->csr_ms = now_ms() - t0;
   } catch (const Error &e) {
     g_create_error = e.msg;
@@ -756,6 +764,12 @@ louvain_status louvain_run(louvain_t h) {
   } catch (const Error &e) {
     return fail(h, e);
   }
+  return LV_OK;
+}
+
+louvain_status louvain_weight_scale(louvain_t h, int32_t *s) {
+  if (!h || !s) return LV_EINVAL;
+  *s = h->wscale;
   return LV_OK;
 }
 

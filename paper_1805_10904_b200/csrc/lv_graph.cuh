@@ -116,6 +116,76 @@ inline i64 d2h_i64(Ctx &c, const i64 *p) {
   return v;
 }
 
+// ------------------------------------------------- real weights
+// The paper stores float weights.  Reading D28 maps them to fixed-point
+// integers w~ = rint(w * 2^s) (round half to even; w * 2^s is an exact power-of-two
+// scaling in binary64), s the largest integer with T(s) = sum_k w~_k <= 2^52, and runs
+// the integer method on w~: exact, schedule-independent sums and scores as for integer
+// graphs, and Q of the fixed-point graph within m * 2^-s (relative) of the real one.
+template <class T>
+__global__ void __launch_bounds__(256) k_fx_sum(i64 m, const T *__restrict__ w, int s, u64 *acc, int *bad) {
+  constexpr u64 CAP = (u64)1 << 53;  // anything above 2^52 only needs to be "too big"
+  u64 t = 0;
+  for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
+    const double x = (double)w[k];
+    if (!(x > 0.0) || !isfinite(x)) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    const double f = rint(ldexp(x, s));
+    t += f < (double)CAP ? (u64)f : CAP;
+    t = t < CAP ? t : CAP;
+  }
+  t = block_sum_u64<256>(t);  // <= 256 * 2^53
+  if (threadIdx.x == 0 && t) atomicAdd(acc, t < CAP ? t : CAP);  // <= 1024 blocks * 2^53
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_fx_conv(i64 m, const T *__restrict__ w, int s, i64 *out, int *bad) {
+  for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
+    const i64 q = (i64)rint(ldexp((double)w[k], s));
+    if (q <= 0) atomicOr(bad, 2);  // dynamic range beyond the 52-bit budget
+    out[k] = q;
+  }
+}
+
+// Quantise m real weights (in_wt LV_W_F32 / LV_W_F64, device pointer) into out (int64).
+// Returns s.  Errors: LV_EGRAPH for a weight that is not finite and > 0, or that rounds
+// to 0 at s.
+inline int quantize_real(Ctx &c, i64 m, const void *w, int in_wt, Buf<i64> &out) {
+  out.alloc(c.A, m > 0 ? m : 1);
+  if (m == 0) return 0;
+  Buf<u64> t(c.A, 2);
+  int *bad = (int *)(t.p + 1);
+  const unsigned gm = std::min(grid_for(c, m), 1024u);
+  const u64 lim = (u64)1 << 52;
+  auto T = [&](int s) {
+    LV_CUDA(cudaMemsetAsync(t.p, 0, 2 * sizeof(u64), c.s));
+    if (in_wt == LV_W_F32) LV_LAUNCH(c, k_fx_sum<float>, gm, 256, 0, m, (const float *)w, s, t.p, bad);
+    else LV_LAUNCH(c, k_fx_sum<double>, gm, 256, 0, m, (const double *)w, s, t.p, bad);
+    u64 h[2];
+    LV_CUDA(cudaMemcpyAsync(h, t.p, sizeof(h), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    LV_REQUIRE((int)h[1] == 0, LV_EGRAPH, "real weight not finite and > 0 (P:L43: positive weights)");
+    return h[0];
+  };
+  // T is non-decreasing in s: binary search the largest s with T(s) <= 2^52
+  int lo = -1100, hi = 1100;  // T(lo) = 0 <= 2^52 < T(hi) for any m >= 1 positive weights
+  while (hi - lo > 1) {
+    const int mid = lo + (hi - lo) / 2;
+    if (T(mid) <= lim) lo = mid;
+    else hi = mid;
+  }
+  LV_CUDA(cudaMemsetAsync(t.p, 0, 2 * sizeof(u64), c.s));
+  if (in_wt == LV_W_F32) LV_LAUNCH(c, k_fx_conv<float>, grid_for(c, m), 256, 0, m, (const float *)w, lo, out.p, bad);
+  else LV_LAUNCH(c, k_fx_conv<double>, grid_for(c, m), 256, 0, m, (const double *)w, lo, out.p, bad);
+  u64 h[2];
+  LV_CUDA(cudaMemcpyAsync(h, t.p, sizeof(h), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  LV_REQUIRE((int)h[1] == 0, LV_EGRAPH, "real weights span more than the 52-bit fixed-point budget (reading D28)");
+  return lo;
+}
+
 // Build the level-0 CSR from device COO records.  Returns LV_OK / LV_EGRAPH / LV_EZEROW
 // through exceptions.  in_wt: 0 none, 1 int32, 2 int64 (louvain_wtype).
 inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *dst, const void *w, int in_wt,

@@ -146,6 +146,14 @@ def rmat(scale=24, edge_factor=16, a=0.57, b=0.19, c=0.19, wmax=16, seed=4) -> R
                    meta=dict(scale=scale, edge_factor=edge_factor, wmax=wmax, seed=seed))
 
 
+def real_weights(m: int, seed: int, sigma: float = 1.0, dtype=np.float32) -> np.ndarray:
+    """Seeded positive real weights (lognormal(0, sigma), numpy's counter-based Philox
+    bit generator) for the float-weight mode (the paper stores float
+    weights).  Input data only: no method arithmetic."""
+    g = np.random.Generator(np.random.Philox(key=int(seed)))
+    return g.lognormal(0.0, float(sigma), int(m)).astype(dtype)
+
+
 # The five BASELINE.json configurations (and the small analogues used by parity tests).
 CONFIGS = {
     "karate": lambda: karate(),

@@ -114,11 +114,13 @@ class Louvain:
                 g.w, g.wtype = None, _lib.LV_W_NONE
             else:
                 ww = w.contiguous()
-                if ww.dtype not in (t.int32, t.int64):
-                    raise TypeError("weights must be int32 or int64 (integer-exact path)")
+                kinds = {t.int32: _lib.LV_W_I32, t.int64: _lib.LV_W_I64, t.float32: _lib.LV_W_F32,
+                         t.float64: _lib.LV_W_F64}
+                if ww.dtype not in kinds:
+                    raise TypeError("weights must be int32/int64 (exact) or float32/float64 (fixed point, D28)")
                 self._keep.append(ww)
                 g.w = ww.data_ptr()
-                g.wtype = _lib.LV_W_I32 if ww.dtype == t.int32 else _lib.LV_W_I64
+                g.wtype = kinds[ww.dtype]
         else:
             s = np.ascontiguousarray(src, dtype=np.int32)
             d = np.ascontiguousarray(dst, dtype=np.int32)
@@ -129,14 +131,18 @@ class Louvain:
                 g.w, g.wtype = None, _lib.LV_W_NONE
             else:
                 ww = np.ascontiguousarray(w)
-                if ww.dtype not in (np.int32, np.int64):
-                    if np.all(ww == np.round(ww)):
+                kinds = {np.dtype(np.int32): _lib.LV_W_I32, np.dtype(np.int64): _lib.LV_W_I64,
+                         np.dtype(np.float32): _lib.LV_W_F32, np.dtype(np.float64): _lib.LV_W_F64}
+                if ww.dtype not in kinds:
+                    if ww.dtype.kind in "iu":
                         ww = ww.astype(np.int64)
+                    elif ww.dtype.kind == "f":
+                        ww = ww.astype(np.float64)
                     else:
-                        raise TypeError("weights must be integers (integer-exact path)")
+                        raise TypeError("weights must be integers (exact) or reals (fixed point, D28)")
                 self._keep.append(ww)
                 g.w = ww.ctypes.data
-                g.wtype = _lib.LV_W_I32 if ww.dtype == np.int32 else _lib.LV_W_I64
+                g.wtype = kinds[ww.dtype]
         rc = self._lib.louvain_create(C.byref(g), C.byref(cfg), C.byref(self._h))
         self._keep = [k for k in self._keep if not isinstance(k, np.ndarray)]
         check(rc, None)
@@ -165,6 +171,13 @@ class Louvain:
     def run(self):
         check(self._lib.louvain_run(self._h), self._h)
         return self
+
+    @property
+    def weight_scale(self) -> int:
+        """s of the real-weight fixed point w~ = rint(w·2^s) (reading D28); 0 for integers."""
+        x = C.c_int32()
+        check(self._lib.louvain_weight_scale(self._h, C.byref(x)), self._h)
+        return x.value
 
     @property
     def num_levels(self) -> int:
