@@ -58,6 +58,8 @@ class _Config(C.Structure):
         ("merge_isolated", C.c_int32),
         ("theta_schedule", C.POINTER(C.c_double)),
         ("theta_schedule_len", C.c_int32),
+        ("coloring", C.c_int32),
+        ("color_classes", C.c_int32),
     ]
 
 
@@ -87,6 +89,12 @@ def _L():
         lib.og_decide.restype = i32
         lib.og_sweep.argtypes = [GP, P, P, i32]
         lib.og_sweep.restype = i64
+        lib.og_color_priority.argtypes = [i64]
+        lib.og_color_priority.restype = C.c_uint64
+        lib.og_color.argtypes = [GP, P]
+        lib.og_color.restype = i32
+        lib.og_sweep_colored.argtypes = [GP, P, i32, P, P]
+        lib.og_sweep_colored.restype = i64
         lib.og_renumber.argtypes = [i64, P, P]
         lib.og_renumber.restype = i64
         lib.og_induce.argtypes = [GP, P, i64, C.POINTER(GP)]
@@ -205,6 +213,23 @@ class Graph:
         finally:
             _L().og_state_free(st)
 
+    def color(self):
+        """Greedy distance-1 colouring by decreasing priority (D29) -> (colors, K)."""
+        out = np.empty(self.n, dtype=np.int32)
+        K = _L().og_color(self._h, _ptr(out))
+        if K < 0:
+            raise OracleError("og_color failed")
+        return out, int(K)
+
+    def sweep_colored(self, labels, colors, K):
+        lab = np.ascontiguousarray(labels, dtype=np.int32)
+        col = np.ascontiguousarray(colors, dtype=np.int32)
+        out = np.empty_like(lab)
+        moved = _L().og_sweep_colored(self._h, _ptr(col), int(K), _ptr(lab), _ptr(out))
+        if moved < 0:
+            raise OracleError("og_sweep_colored failed")
+        return out, int(moved)
+
     def induce(self, labels, k) -> "Graph":
         lab = np.ascontiguousarray(labels, dtype=np.int32)
         h = C.POINTER(_Graph)()
@@ -238,14 +263,21 @@ class Result:
     edge_visits: int = 0
 
 
+def color_priority(v: int) -> int:
+    return int(_L().og_color_priority(int(v)))
+
+
 def run(graph: Graph, theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64,
-        stop_rule=0, merge_isolated=True, theta_schedule=None) -> Result:
+        stop_rule=0, merge_isolated=True, theta_schedule=None, coloring=False,
+        color_classes=32) -> Result:
     """Algorithm 2 around Algorithm 1 with the DESIGN.md readings."""
     cfg = _Config()
     _L().og_config_default(C.byref(cfg))
     cfg.theta, cfg.big_theta = float(theta), float(big_theta)
     cfg.max_sweeps, cfg.max_levels = int(max_sweeps), int(max_levels)
     cfg.stop_rule, cfg.merge_isolated = int(stop_rule), int(bool(merge_isolated))
+    cfg.coloring = int(bool(coloring))
+    cfg.color_classes = int(color_classes)
     sched = None
     if theta_schedule:
         sched = (C.c_double * len(theta_schedule))(*theta_schedule)

@@ -44,6 +44,8 @@ void og_config_default(og_config *c) {
     c->merge_isolated = 1;    /* D14 */
     c->theta_schedule = NULL; /* D21 */
     c->theta_schedule_len = 0;
+    c->coloring = 0;          /* D29: off (the paper's pure Jacobi sweeps) */
+    c->color_classes = 32;    /* D29: colours >= 31 share the last class */
 }
 
 /* ------------------------------------------------------- graph construction */
@@ -280,6 +282,66 @@ int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_ou
     return moved;
 }
 
+/* ------------------------------------------------- colouring heuristic (F2, D29) */
+
+uint64_t og_color_priority(int64_t v) {
+    uint64_t k = (uint64_t)v ^ 0x9E3779B97F4A7C15ull;
+    k ^= k >> 33; k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+typedef struct { uint64_t p; int32_t v; } prio_t;
+static int prio_desc(const void *a, const void *b) {
+    uint64_t x = ((const prio_t *)a)->p, y = ((const prio_t *)b)->p;
+    return x < y ? 1 : x > y ? -1 : 0;
+}
+
+int32_t og_color(const og_graph *g, int32_t *color) {
+    int64_t n = g->n;
+    prio_t *ord = (prio_t *)malloc((size_t)n * sizeof(prio_t));
+    uint8_t *used = (uint8_t *)calloc((size_t)n + 1, 1);
+    if (!ord || !used) { free(ord); free(used); return -1; }
+    for (int64_t v = 0; v < n; ++v) { ord[v].p = og_color_priority(v); ord[v].v = (int32_t)v; color[v] = -1; }
+    qsort(ord, (size_t)n, sizeof(prio_t), prio_desc);
+    int32_t K = 0;
+    for (int64_t t = 0; t < n; ++t) {
+        int32_t v = ord[t].v;
+        for (int64_t e = g->row_ptr[v]; e < g->row_ptr[v + 1]; ++e)      /* mark */
+            if (color[g->col[e]] >= 0) used[color[g->col[e]]] = 1;
+        int32_t c = 0;
+        while (used[c]) ++c;                                              /* smallest free */
+        color[v] = c;
+        if (c + 1 > K) K = c + 1;
+        for (int64_t e = g->row_ptr[v]; e < g->row_ptr[v + 1]; ++e)      /* unmark */
+            if (color[g->col[e]] >= 0) used[color[g->col[e]]] = 0;
+        used[c] = 0;
+    }
+    free(ord); free(used);
+    return K;
+}
+
+int64_t og_sweep_colored(const og_graph *g, const int32_t *color, int32_t ncolors,
+                         const int32_t *labels_in, int32_t *labels_out) {
+    int64_t n = g->n, moved = 0;
+    int32_t *cur = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!cur) return -1;
+    memcpy(cur, labels_in, (size_t)n * sizeof(int32_t));
+    memcpy(labels_out, labels_in, (size_t)n * sizeof(int32_t));
+    for (int32_t c = 0; c < ncolors; ++c) {
+        og_state *st = og_state_new(g, cur);              /* state after class c-1 */
+        if (!st) { free(cur); return -1; }
+        for (int64_t i = 0; i < n; ++i)
+            if (color[i] == c) labels_out[i] = og_decide(st, i, 0);
+        og_state_free(st);
+        memcpy(cur, labels_out, (size_t)n * sizeof(int32_t));   /* commit class c */
+    }
+    for (int64_t i = 0; i < n; ++i) moved += labels_out[i] != labels_in[i];
+    free(cur);
+    return moved;
+}
+
 /* ---------------------------------------------------------------- modularity */
 
 /* Eq. 3: Q = (1/2W) Σ_i e_{i→C(i)} − Σ_C (deg_C/2W)², with e_{i→C(i)} counting a loop
@@ -416,13 +478,23 @@ static int one_level(const og_graph *g, const og_config *cfg, double theta, int3
     L->qs = (double *)malloc((size_t)(cfg->max_sweeps + 1) * sizeof(double));
     if (!next || !deg || !L->moved || !L->qs) { free(next); free(deg); return OG_ENOMEM; }
     for (int64_t i = 0; i < n; ++i) C[i] = (int32_t)i;   /* initStatus: singletons */
+    int32_t *color = NULL, K = 0;
+    if (cfg->coloring) {                                  /* D29: colour the level graph */
+        color = (int32_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+        if (!color || (K = og_color(g, color)) < 0) { free(color); free(next); free(deg); return OG_ENOMEM; }
+        if (cfg->color_classes > 0 && K > cfg->color_classes) {   /* D29 class cap */
+            K = cfg->color_classes;
+            for (int64_t i = 0; i < n; ++i) if (color[i] > K - 1) color[i] = K - 1;
+        }
+    }
     int first = 1;                                        /* Q_prev ← −∞ (D11) */
     double Qp = 0.0;
     int32_t s;
     L->trace_len = 0;
     for (s = 1; s <= cfg->max_sweeps; ++s) {              /* D12 cap */
-        int64_t moved = og_sweep(g, C, next, 0);          /* decisions from the snapshot */
-        if (moved < 0) { free(next); free(deg); return OG_ENOMEM; }
+        int64_t moved = cfg->coloring ? og_sweep_colored(g, color, K, C, next)   /* D29 */
+                                      : og_sweep(g, C, next, 0);   /* decisions from the snapshot */
+        if (moved < 0) { free(color); free(next); free(deg); return OG_ENOMEM; }
         *visits += g->nnz;
         memcpy(C, next, (size_t)n * sizeof(int32_t));     /* commit (D13) */
         for (int64_t c = 0; c < n; ++c) deg[c] = 0;
@@ -443,7 +515,7 @@ static int one_level(const og_graph *g, const og_config *cfg, double theta, int3
         og_sweep(g, C, next, 1);
         memcpy(C, next, (size_t)n * sizeof(int32_t));
     }
-    free(next); free(deg);
+    free(color); free(next); free(deg);
     return OG_OK;
 }
 

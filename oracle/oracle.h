@@ -51,6 +51,8 @@ typedef struct {
     int32_t merge_isolated;   /* D14 default 1                                */
     const double *theta_schedule; /* D21 threshold cycling; NULL = constant θ */
     int32_t theta_schedule_len;
+    int32_t coloring;         /* F2 / D29: 1 = sweep colour classes in turn         */
+    int32_t color_classes;    /* D29: classes = min(colour, color_classes-1); 0 = all */
 } og_config;
 
 /* error codes (0 = ok) */
@@ -93,6 +95,22 @@ int32_t   og_decide(const og_state *st, int64_t i, int32_t mode);
 /* One Jacobi sweep (mode 0) or one merge batch (mode 1) over all vertices from the
  * snapshot labels_in; writes labels_out; returns the number of vertices that moved. */
 int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_out, int32_t mode);
+
+/* SURVEY §8(f) F2, reading D29 — Lu et al.'s distance-1 colouring heuristic (the
+ * "other heuristics" of P:L89 / P:L441).
+ * og_color_priority: π(v) = fmix64(v XOR 0x9E3779B97F4A7C15) (MurmurHash3 finaliser, a
+ *   bijection on 64-bit words, so priorities are distinct).
+ * og_color: greedy colouring in order of decreasing π: colour(v) = the smallest c >= 0
+ *   not used by an already coloured neighbour (loops ignored) — the colouring Jones-
+ *   Plassmann rounds produce with these priorities.  Returns the number of colours.
+ * og_sweep_colored: one sweep = the colour classes 0..K-1 in turn; the vertices of a
+ *   class decide in parallel (og_decide, Jacobi within the class — no two of them are
+ *   adjacent) against the state left by the previous class, whose moves are committed
+ *   before the next class starts.  Returns the number of vertices that moved. */
+uint64_t og_color_priority(int64_t v);
+int32_t  og_color(const og_graph *g, int32_t *color);
+int64_t  og_sweep_colored(const og_graph *g, const int32_t *color, int32_t ncolors,
+                          const int32_t *labels_in, int32_t *labels_out);
 
 /* Order-preserving dense renumbering (D18).  Returns k. */
 int64_t og_renumber(int64_t n, const int32_t *labels_in, int32_t *labels_out);
