@@ -94,6 +94,14 @@ typedef struct {
     void *nccl_comm;         /* ncclComm_t for the sweep-sharded path; NULL = 1 GPU     */
     int32_t rank, world;     /* this process's rank / world size in nccl_comm           */
     int32_t profile;         /* 1: time every sweep kernel with CUDA events during run   */
+    int32_t coloring;        /* SURVEY F2, reading D29 (Lu et al.'s colouring heuristic,
+                                P:L89 / P:L441 "other heuristics"): 1 = colour each level
+                                (distance-1, greedy by fmix64 priority) and sweep the colour
+                                classes in turn, each against the state the previous class
+                                committed; default 0 (the paper's synchronous sweeps).
+                                Not available in the sweep-sharded mode (LV_EINVAL).       */
+    int32_t color_classes;   /* D29: colours >= color_classes-1 share the last class
+                                (swept synchronously); 0 = one class per colour; default 32 */
 } louvain_config;
 
 /* Fill `cfg` with the defaults above. */
@@ -141,6 +149,11 @@ louvain_status louvain_level_stats(louvain_t h, int32_t level, int32_t *sweeps, 
  * kernel launches the handle issued since louvain_create (CSR build + every run). */
 louvain_status louvain_run_stats(louvain_t h, int64_t *edge_visits, int64_t *launches);
 
+/* Colouring heuristic (cfg.coloring, D29) statistics of a recorded level: number of
+ * colours of the level graph (before the color_classes cap) and Jones–Plassmann rounds.
+ * Both 0 when colouring was off.  Errors: LV_ESTATE before run, LV_ERANGE bad level. */
+louvain_status louvain_level_colors(louvain_t h, int32_t level, int32_t *colors, int32_t *rounds);
+
 /* ---- step-level entry points (tests, benchmarks).  Each operates on level 0 of the
  * handle's graph and leaves louvain_run's results untouched. ---- */
 
@@ -151,6 +164,11 @@ louvain_status louvain_run_stats(louvain_t h, int64_t *edge_visits, int64_t *lau
 louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *labels_out,
                              int32_t mode, int32_t on_device, int64_t *moved, int64_t *i2,
                              int64_t *s2_hi, uint64_t *s2_lo);
+
+/* Distance-1 colouring of the level-0 graph (D29): colors[v] (length n, host or device)
+ * = the greedy colour in decreasing fmix64(v ^ 0x9E3779B97F4A7C15) order, computed by
+ * Jones–Plassmann rounds; *ncolors = number of colours.  Errors: LV_EINVAL. */
+louvain_status louvain_color(louvain_t h, int32_t *colors, int32_t on_device, int32_t *ncolors);
 
 /* Time `reps` consecutive level-0 sweeps (each: all bin kernels + commit) from the
  * all-singleton state after `warm` untimed ones, with CUDA events on the handle stream.

@@ -19,7 +19,7 @@ LV_W_NONE, LV_W_I32, LV_W_I64, LV_W_F32, LV_W_F64 = 0, 1, 2, 3, 4
 
 EXPORTS = [
     "louvain_config_default", "louvain_create", "louvain_run", "louvain_num_levels", "louvain_level_size",
-    "louvain_get_partition", "louvain_modularity", "louvain_weight_scale", "louvain_level_stats", "louvain_run_stats", "louvain_sweep",
+    "louvain_get_partition", "louvain_modularity", "louvain_weight_scale", "louvain_level_colors", "louvain_color", "louvain_level_stats", "louvain_run_stats", "louvain_sweep",
     "louvain_time_sweeps", "louvain_profile_json", "louvain_get_csr", "louvain_contract", "louvain_last_error", "louvain_destroy",
     "louvain_nccl_unique_id", "louvain_nccl_init", "louvain_nccl_destroy", "louvain_shard_bounds",
 ]
@@ -59,6 +59,8 @@ class Config(C.Structure):
         ("rank", C.c_int32),
         ("world", C.c_int32),
         ("profile", C.c_int32),
+        ("coloring", C.c_int32),
+        ("color_classes", C.c_int32),
     ]
 
 
@@ -88,6 +90,8 @@ def load() -> C.CDLL:
         "louvain_run": ([P], C.c_int),
         "louvain_num_levels": ([P, C.POINTER(i32)], C.c_int),
         "louvain_weight_scale": ([P, C.POINTER(i32)], C.c_int),
+        "louvain_level_colors": ([P, i32, C.POINTER(i32), C.POINTER(i32)], C.c_int),
+        "louvain_color": ([P, P, i32, C.POINTER(i32)], C.c_int),
         "louvain_level_size": ([P, i32, C.POINTER(i64)], C.c_int),
         "louvain_get_partition": ([P, i32, P, i64, i32], C.c_int),
         "louvain_modularity": ([P, i32, C.POINTER(dbl)], C.c_int),

@@ -89,6 +89,8 @@ struct AggArgs {
   u64 *counters;           // SWEEP/MERGE: [0] I2 [1] moved [2] S2 lo [3] S2 hi [4] cand
   const Chunk *chunks;     // hub path: HUB_CHUNK-edge chunks of the hub rows
   int hint;                // bit0: evict_first on streams; bit1: evict_last on gathers
+  int coloring;            // 1: a colour-class pass (D29): counters [0] Σ e_own and [2,3]
+                           //   Σ 2W·e_best over the MOVED vertices (ΔI2 of the class)
 };
 
 __device__ __forceinline__ void store_w(const AggArgs &a, i64 o, u64 v) {
@@ -447,8 +449,17 @@ __device__ __forceinline__ void sweep_decide(const AggArgs &a, Acc &acc, int32_t
   a.label_next[r] = tgt;
   if (tgt != own) record_move(a, own, tgt, di);
   acc.moved += (tgt != own);
-  acc.i2 += eown;
-  acc.add_sq(dr);  // deg of label index r: Σ over all labels gives S2
+  if (!a.coloring) {
+    acc.i2 += eown;
+    acc.add_sq(dr);  // deg of label index r: Σ over all labels gives S2
+  } else if (tgt != own) {
+    // ΔI2 of a class (D29): a move own -> tgt changes I2 by 2(e_{i->tgt} - e_{i->own})
+    // (its non-adjacent classmates add independently).  2W·e_{i->tgt} = S(best) + δ_i·deg_tgt
+    // exactly; summed in 128 bits, divided by 2W once on the host.
+    acc.i2 += eown;
+    const i128 t = (S64 ? (i128)(i64)best.lo : cand_S(best)) + (i128)di * (i128)load_deg(a, tgt);
+    add128(acc.s2hi, acc.s2lo, (u64)((u128)t >> 64), (u64)t);
+  }
 }
 
 // Score candidate (packed key k, e_{i->C} = v, deg_C = dk) into best.

@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "lv_color.cuh"
 #include "lv_graph.cuh"
 
 using namespace lv;
@@ -147,6 +148,7 @@ struct LevelRec {
   Buf<int32_t> labels;  // dense, values in [0, n_{l+1})
   double q = 0;
   int32_t sweeps = 0;
+  int32_t colors = 0, color_rounds = 0;  // colouring heuristic (D29): colours, JP rounds
   double times[5] = {0, 0, 0, 0, 0};
 };
 
@@ -300,12 +302,16 @@ Plan plan_of(Bins &B) {  // unsharded view of existing bins (step-level entry po
 }
 
 // Run one pass of MODE (snapshot st.lab[cur] -> st.lab[cur^1], deg/size -> next buffers).
+// colored: a colour-class pass (D29) — only the class's rows are binned in P, so the other
+// rows' labels are carried into the next buffer first; counters hold the class's ΔI2 terms.
+// colored passes accumulate into the caller's (zeroed) counter block cctr and return
+// without a host sync (the caller reads all classes' counters once per sweep).
 SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int mode, KTimer *tm = nullptr,
-                  std::vector<SweepOut> *per_bin = nullptr) {
+                  std::vector<SweepOut> *per_bin = nullptr, bool colored = false, u64 *cctr = nullptr) {
   Ctx &c = h->c;
   const int nloc = (int)P.parts.size();
   const size_t SLOT = (size_t)NBIN * 8;
-  LV_CUDA(cudaMemsetAsync(h->dctr.p, 0, (size_t)nloc * SLOT * sizeof(u64), c.s));
+  if (!colored) LV_CUDA(cudaMemsetAsync(h->dctr.p, 0, (size_t)nloc * SLOT * sizeof(u64), c.s));
   AggArgs a;
   memset(&a, 0, sizeof(a));
   a.ptr = g.row_ptr.p;
@@ -323,6 +329,10 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   a.size_next = P.sharded ? nullptr : size_next;
   if (tm && mode == M_SWEEP) tm->begin(c.s, "sweep_pass");
   if (tm) tm->begin(c.s, "next_state_copy");
+  if (colored) {
+    LV_CUDA(cudaMemcpyAsync(a.label_next, label, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
+    a.coloring = 1;
+  }
   LV_CUDA(cudaMemcpyAsync(deg_next, a.deg, (size_t)g.n * sizeof(i64), cudaMemcpyDeviceToDevice, c.s));
   LV_CUDA(cudaMemcpyAsync(size_next, size, (size_t)g.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.s));
   if (tm) tm->end(c.s);
@@ -344,7 +354,7 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   }
   const bool narrow = g.max_delta < ((i64)1 << 32);  // e_{i->C} <= δ_i
   for (int j = 0; j < nloc; ++j) {
-    a.counters = h->dctr.p + (size_t)j * SLOT;
+    a.counters = colored ? cctr : h->dctr.p + (size_t)j * SLOT;
     if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, *P.parts[j], a, tm);
     else launch_agg_wt<M_MERGE>(c, g.wt, narrow, *P.parts[j], a, tm);
   }
@@ -370,6 +380,7 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
     LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, label, a.label_next, g.delta.p, deg_next, size_next);
   LV_LAUNCH(c, k_cpk, grid_for(c, g.n), 256, 0, g.n, deg_next, size_next, st.cpk[st.cur ^ 1].p);
   if (tm && mode == M_SWEEP) tm->end(c.s);
+  if (colored) return SweepOut();
   LV_CUDA(cudaMemcpyAsync(h->hctr, src, (size_t)nsum * SLOT * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
   SweepOut o;
@@ -494,6 +505,97 @@ int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, dou
   return sweeps;
 }
 
+// Colour classes of a level (D29): the level graph coloured by Jones–Plassmann rounds
+// (priorities keyed on the level-graph id: orig maps a compacted position back to it),
+// colours >= cap-1 folded into the last class, and one set of degree bins per class.
+struct ColorPlan {
+  std::vector<std::unique_ptr<Bins>> cls;
+  int32_t colors = 0, rounds = 0;
+  bool capped = false;  // the last class holds every colour >= cap-1 (not independent)
+};
+
+ColorPlan make_color_plan(louvain_ctx *h, const DGraph &g, const int32_t *orig) {
+  Ctx &c = h->c;
+  ColorPlan CP;
+  Buf<int32_t> color;
+  const double t0 = now_ms();
+  CP.colors = color_graph(c, g.n, g.row_ptr.p, g.col.p, orig, color, &CP.rounds);
+  const double t1 = now_ms();
+  int32_t K = CP.colors;
+  const int32_t cap = h->cfg.color_classes;
+  if (cap > 0 && K > cap) {
+    LV_LAUNCH(c, k_cap_classes, grid_for(c, g.n), 256, 0, g.n, color.p, cap);
+    K = cap;
+    CP.capped = true;
+  }
+  for (int32_t k = 0; k < K; ++k) {
+    CP.cls.push_back(std::make_unique<Bins>());
+    build_bins(c, g.row_ptr.p, g.n, g.n, *CP.cls.back(), 0, -1, false, color.p, k);
+  }
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  if (getenv("LV_COLOR_TRACE"))
+    fprintf(stderr, "colour plan: n=%lld colours=%d rounds=%d colour %.1f ms, class bins %.1f ms\n", (long long)g.n,
+            CP.colors, CP.rounds, t1 - t0, now_ms() - t1);
+  return CP;
+}
+
+// Algorithm 1 for one level with the colouring heuristic (D29): a sweep runs the colour
+// classes in turn, committing each class before the next; then Q (Eq. 3) of the committed
+// state from I2 (tracked exactly: I2 = 2Σloop at the singleton start, + the classes' ΔI2)
+// and S2 = Σ_C deg_C² (one pass over deg), and the same stop test as the oracle (D10-D13).
+int32_t one_level_colored(louvain_ctx *h, const DGraph &g, const ColorPlan &CP, State &st, double theta, u64 lsum,
+                          u128 s2i) {
+  Ctx &c = h->c;
+  const louvain_config &cfg = h->cfg;
+  if (cfg.max_sweeps <= 0) return 0;
+  const u128 twoW = (u128)(2 * g.W);
+  i128 I2 = (i128)2 * (i128)lsum;
+  const size_t SLOT = (size_t)NBIN * 8, K = CP.cls.size();
+  // per class one counter block (NBIN slots of 8), then [K*SLOT]: tail ΔI2, [+1..2]: S2
+  Buf<u64> ctr(c.A, K * SLOT + 4);
+  std::vector<u64> hc(K * SLOT + 4);
+  bool first = true;
+  double Qp = 0.0;
+  int32_t s;
+  for (s = 1; s <= cfg.max_sweeps; ++s) {
+    LV_CUDA(cudaMemsetAsync(ctr.p, 0, (K * SLOT + 4) * sizeof(u64), c.s));
+    for (size_t k = 0; k < K; ++k) {
+      const Bins &B = *CP.cls[k];
+      if (B.active() == 0) continue;
+      run_pass(h, g, plan_of(const_cast<Bins &>(B)), st, M_SWEEP, nullptr, nullptr, true, ctr.p + k * SLOT);
+      if (CP.capped && k + 1 == K)  // adjacent movers possible: exact edge pass over the class
+        LV_LAUNCH(c, k_delta_i2, grid_for(c, B.active(), 8), 256, 0, B.active(), B.rows.p, g.row_ptr.p, g.col.p,
+                  (const void *)g.w.p, g.wt, st.lab[st.cur].p, st.lab[st.cur ^ 1].p, ctr.p + K * SLOT);
+      commit(h, g, st);
+    }
+    h->edge_visits += g.nnz;
+    LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, g.n), 256, 0, DegArr{st.deg[st.cur].p}, g.n, ctr.p + K * SLOT + 1);
+    LV_CUDA(cudaMemcpyAsync(hc.data(), ctr.p, hc.size() * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    // independent classes: ΔI2 = 2(Σ e_best − Σ e_own) over the movers, where the kernels
+    // summed Σ e_own (slot 0) and Σ 2W·e_best (slots 2, 3; exact, 128-bit)
+    u64 moved = 0, eo = 0;
+    u128 eb2w = 0;
+    for (size_t k = 0; k < K; ++k)
+      for (int b = 0; b < NBIN; ++b) {
+        const u64 *x = hc.data() + k * SLOT + 8 * b;
+        moved += x[1];
+        if (CP.capped && k + 1 == K) continue;
+        eo += x[0];
+        eb2w += ((u128)x[3] << 64) | x[2];
+      }
+    LV_REQUIRE(eb2w % twoW == 0, LV_ECUDA, "colour-class I2 update is not a multiple of 2W");
+    I2 += (i128)2 * ((i128)(eb2w / twoW) - (i128)eo) + (i128)(i64)hc[K * SLOT];
+    const i128 S2 = (i128)((((u128)hc[K * SLOT + 2] << 64) | hc[K * SLOT + 1]) + s2i);
+    const double Q = q_from(g.W, I2, S2);
+    const bool stop = !first && stop_test(cfg.stop_rule, Q, Qp, theta);
+    first = false;
+    Qp = Q;
+    if (stop || moved == 0) break;
+  }
+  return s > cfg.max_sweeps ? cfg.max_sweeps : s;
+}
+
 // Q of the partition that produced graph hgr: I2 = 2Σloop', S2 = Σδ'² (exact).
 double q_of_contracted(louvain_ctx *h, const DGraph &hg) {
   Ctx &c = h->c;
@@ -537,9 +639,21 @@ void run_impl(louvain_ctx *h) {
     State st;
     init_state(h, gs, st, compacted ? cp.rk.p : nullptr);
     Plan P = make_plan(h, gs);
+    ColorPlan CP;
+    if (cfg.coloring) {
+      Buf<int32_t> orig;
+      if (compacted) {  // position -> rank -> level-graph id
+        orig.alloc(c.A, gs.n);
+        LV_LAUNCH(c, k_gather_i32, grid_for(c, gs.n), 256, 0, gs.n, cp.rk.p, cp.inv.p, orig.p);
+      }
+      CP = make_color_plan(h, gs, compacted ? orig.p : nullptr);
+      rec->colors = CP.colors;
+      rec->color_rounds = CP.rounds;
+    }
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t1 = now_ms();
-    rec->sweeps = one_level(h, gs, P, st, theta, lsum, s2i);
+    rec->sweeps = cfg.coloring ? one_level_colored(h, gs, CP, st, theta, lsum, s2i)
+                               : one_level(h, gs, P, st, theta, lsum, s2i);
     if (cfg.merge_isolated) {
       run_pass(h, gs, P, st, M_MERGE);
       commit(h, gs, st);
@@ -647,6 +761,8 @@ louvain_status louvain_config_default(louvain_config *cfg) {
   cfg->merge_isolated = 1;
   cfg->device = 0;
   cfg->world = 1;
+  cfg->coloring = 0;
+  cfg->color_classes = 32;
   return LV_OK;
 }
 
@@ -663,7 +779,8 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
   if (cfg_in) cfg = *cfg_in;
   else louvain_config_default(&cfg);
   if (cfg.max_sweeps < 1 || cfg.max_levels < 1 || cfg.stop_rule < 0 || cfg.stop_rule > 1 || !(cfg.theta >= 0) ||
-      !(cfg.big_theta == cfg.big_theta) || (cfg.theta_schedule_len > 0 && !cfg.theta_schedule)) {
+      !(cfg.big_theta == cfg.big_theta) || (cfg.theta_schedule_len > 0 && !cfg.theta_schedule) ||
+      cfg.coloring < 0 || cfg.coloring > 1 || cfg.color_classes < 0 || (cfg.coloring && cfg.nccl_comm)) {
     g_create_error = "invalid config";
     return LV_EINVAL;
   }
@@ -820,6 +937,32 @@ louvain_status louvain_level_stats(louvain_t h, int32_t level, int32_t *sweeps, 
   if (sweeps) *sweeps = h->levels[level]->sweeps;
   if (times)
     for (int i = 0; i < 5; ++i) times[i] = h->levels[level]->times[i];
+  return LV_OK;
+}
+
+louvain_status louvain_level_colors(louvain_t h, int32_t level, int32_t *colors, int32_t *rounds) {
+  if (!h) return LV_EINVAL;
+  if (!h->ran) return LV_ESTATE;
+  if (level < 0 || level >= (int32_t)h->levels.size()) return LV_ERANGE;
+  if (colors) *colors = h->levels[level]->colors;
+  if (rounds) *rounds = h->levels[level]->color_rounds;
+  return LV_OK;
+}
+
+louvain_status louvain_color(louvain_t h, int32_t *colors, int32_t on_device, int32_t *ncolors) {
+  if (!h || !colors) return LV_EINVAL;
+  try {
+    Ctx &c = h->c;
+    LV_CUDA(cudaSetDevice(c.device));
+    Buf<int32_t> col;
+    const int32_t K = color_graph(c, h->g0.n, h->g0.row_ptr.p, h->g0.col.p, nullptr, col);
+    LV_CUDA(cudaMemcpyAsync(colors, col.p, h->g0.n * sizeof(int32_t),
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    if (ncolors) *ncolors = K;
+  } catch (const Error &e) {
+    return fail(h, e);
+  }
   return LV_OK;
 }
 

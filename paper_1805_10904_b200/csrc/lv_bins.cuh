@@ -96,9 +96,11 @@ struct LenOf {
   __device__ __forceinline__ i64 operator()(i64 r) const { return ptr[r + 1] - ptr[r]; }
 };
 
-__global__ void k_bin_ids(i64 n, const i64 *__restrict__ ptr, uint8_t *ids, i64 lo, i64 hi) {
+// cls (may be NULL): keep only rows of colour class ck (the colouring heuristic, D29)
+__global__ void k_bin_ids(i64 n, const i64 *__restrict__ ptr, uint8_t *ids, i64 lo, i64 hi,
+                          const int32_t *__restrict__ cls, int32_t ck) {
   for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256)
-    ids[r] = (r >= lo && r < hi) ? (uint8_t)bin_of(ptr[r + 1] - ptr[r]) : (uint8_t)255;
+    ids[r] = (r >= lo && r < hi && (!cls || cls[r] == ck)) ? (uint8_t)bin_of(ptr[r + 1] - ptr[r]) : (uint8_t)255;
 }
 
 // Edge-balanced contiguous vertex ranges (sweep-sharded mode):
@@ -169,12 +171,12 @@ inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
 // Only rows in [lo, hi) are binned (hi < 0: all rows).  rows_only: just B.rows / B.off
 // (the per-bin row lists, ascending within a bin), no headers, edge counts or hub tables.
 inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B, i64 lo = 0, i64 hi = -1,
-                       bool rows_only = false) {
+                       bool rows_only = false, const int32_t *cls = nullptr, int32_t ck = 0) {
   B.nrows = nrows;
   if (hi < 0) hi = nrows;
   Buf<uint8_t> ids(c.A, nrows > 0 ? nrows : 1);
   Buf<i64> pos(c.A, nrows + 1);
-  LV_LAUNCH(c, k_bin_ids, grid_for(c, nrows), 256, 0, nrows, ptr, ids.p, lo, hi);
+  LV_LAUNCH(c, k_bin_ids, grid_for(c, nrows), 256, 0, nrows, ptr, ids.p, lo, hi, cls, ck);
   // counts per bin
   std::vector<i64> cnt(NBIN, 0);
   for (int b = 0; b < NBIN; ++b) {

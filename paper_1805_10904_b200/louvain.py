@@ -80,14 +80,16 @@ class Louvain:
 
     def __init__(self, n, src, dst, w=None, *, device=0, stream=None, torch_allocator=True,
                  theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64, stop_rule=0,
-                 merge_isolated=True, theta_schedule=None, nccl_comm=None, rank=0, world=1, profile=False):
+                 merge_isolated=True, theta_schedule=None, nccl_comm=None, rank=0, world=1, profile=False,
+                 coloring=False, color_classes=32):
         self._lib = _lib.load()
         self._h = C.c_void_p()
         self._keep = []
         cfg = default_config(theta=float(theta), big_theta=float(big_theta), max_sweeps=int(max_sweeps),
                              max_levels=int(max_levels), stop_rule=int(stop_rule),
                              merge_isolated=int(bool(merge_isolated)), device=int(device), rank=int(rank),
-                             world=int(world), profile=int(bool(profile)))
+                             world=int(world), profile=int(bool(profile)), coloring=int(bool(coloring)),
+                             color_classes=int(color_classes))
         if theta_schedule:
             arr = (C.c_double * len(theta_schedule))(*[float(x) for x in theta_schedule])
             self._keep.append(arr)
@@ -178,6 +180,19 @@ class Louvain:
         x = C.c_int32()
         check(self._lib.louvain_weight_scale(self._h, C.byref(x)), self._h)
         return x.value
+
+    def level_colors(self, level: int):
+        """(colours, Jones–Plassmann rounds) of a level under cfg.coloring (D29)."""
+        k, r = C.c_int32(), C.c_int32()
+        check(self._lib.louvain_level_colors(self._h, int(level), C.byref(k), C.byref(r)), self._h)
+        return k.value, r.value
+
+    def color(self):
+        """Distance-1 colouring of the level-0 graph (D29) -> (colors int32[n], K)."""
+        out = np.empty(self.n, dtype=np.int32)
+        k = C.c_int32()
+        check(self._lib.louvain_color(self._h, out.ctypes.data, 0, C.byref(k)), self._h)
+        return out, k.value
 
     @property
     def num_levels(self) -> int:
