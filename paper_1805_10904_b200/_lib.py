@@ -82,7 +82,8 @@ def load() -> C.CDLL:
     if not os.path.exists(SO_PATH):
         raise ImportError(f"liblouvain.so not built ({SO_PATH}); run `python -m paper_1805_10904_b200.build` "
                           "(there is no CPU fallback)")
-    lib = C.CDLL(SO_PATH, mode=C.RTLD_GLOBAL)
+    # LV_SO: an alternative in-tree build of the same library (tuning experiments)
+    lib = C.CDLL(os.environ.get("LV_SO", SO_PATH), mode=C.RTLD_GLOBAL)
     P, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
     sig = {
         "louvain_config_default": ([C.POINTER(Config)], C.c_int),

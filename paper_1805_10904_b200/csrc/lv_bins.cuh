@@ -319,7 +319,8 @@ void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   i64 grid = cdiv(a.nrows, GPB);
   // the pipelined kernel at G = 8, 16 is persistent (one resident wave: many rows per
   // group keep the pipeline full; measured faster), otherwise up to 8 waves
-  i64 cap = (i64)c.sms * occ * ((MODE == M_SWEEP && pipe && G >= 8) ? 1 : 8);
+  static const int w4 = getenv("LV_REG_WAVES4") ? atoi(getenv("LV_REG_WAVES4")) : 8;  // experiments
+  i64 cap = (i64)c.sms * occ * ((MODE == M_SWEEP && pipe && G >= 8) ? 1 : (G == 4 ? w4 : 8));
   if (grid > cap) grid = cap;
   if (tm) tm->begin(st, tag);
   LV_LAUNCH_ON(c, st, kern, (unsigned)grid, BLOCK, 0, a);
