@@ -237,13 +237,22 @@ def main():
     infos = []
     e0.record(stream)
     for _ in range(args.steps):
-        infos.append(step(profile=True))
+        infos.append(step())
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     ms = allmax(ms, world)
+    # per-kernel CUDA events (on each kernel's launching stream) cost host time per launch,
+    # so they run in one extra step after the timed ones, itself timed for the shares
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    pinfo = step(profile=True)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_ms = p0.elapsed_time(p1)
     visits = infos[-1]["edge_visits"]  # of the whole graph (every rank reports the same)
     value = visits / (ms / 1e3)
 
@@ -295,7 +304,7 @@ def main():
     # roofline of the dominant kernel over the timed region
     pk = peaks()
     agg = {}
-    for inf in infos:
+    for inf in [pinfo]:
         for k in inf.get("profile", {"kernels": []})["kernels"]:
             a = agg.setdefault(k["name"], [0.0, 0.0, 0.0])
             a[0] += k["ms"]
@@ -305,7 +314,7 @@ def main():
     top = max(agg, key=lambda k: agg[k][0]) if agg else None
     t_ms, t_bytes, t_launch = agg[top] if agg else (float("nan"), float("nan"), 1.0)
     achieved = t_bytes / (t_ms / 1e3) / 1e9
-    sweep_ms = (sweep_pass[0] / args.steps) if sweep_pass else None
+    sweep_ms = sweep_pass[0] if sweep_pass else None
     traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):  # DRAM bytes of one ncu --set full capture of this kernel
@@ -320,15 +329,16 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note, "kernel": top,
                 "kernel_ms_per_launch": t_ms / t_launch, "alg_bytes_per_launch": t_bytes / t_launch,
-                "kernel_share_of_step": t_ms / args.steps / ms, "peak_source": pk["source"],
-                "note": "per-kernel times: CUDA events on each kernel's launching stream over the timed steps; "
+                "kernel_share_of_step": t_ms / prof_ms, "profiled_step_ms": prof_ms, "peak_source": pk["source"],
+                "note": "per-kernel times: CUDA events on each kernel's launching stream during one profiled step "
+                        "run right after the timed steps (same workload; events cost host time per launch); "
                         "achieved = algorithmic bytes (DESIGN.md §6) / time, averaged over all levels' launches"}
     sweep_roof = None
     if sweep_pass:
         sp_ms, sp_bytes, sp_n = sweep_pass
         sweep_roof = {"achieved": sp_bytes / (sp_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": sp_bytes / (sp_ms / 1e3) / 1e9 / pk["hbm_gbs"], "ms_per_sweep": sp_ms / sp_n,
-                      "alg_bytes_per_sweep": sp_bytes / sp_n, "sweeps": sp_n / args.steps}
+                      "alg_bytes_per_sweep": sp_bytes / sp_n, "sweeps": sp_n}
 
     if rank != 0:
         return 0

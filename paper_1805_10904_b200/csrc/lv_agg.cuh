@@ -975,6 +975,82 @@ __global__ void __launch_bounds__(BLOCK, LV_REGP_MINB) k_sweep_reg(AggArgs a) {
   acc.flush(a.counters);
 }
 
+// ----------------------------------------------------------------- thread per row
+// SWEEP for rows of at most L entries (L <= 8): one thread per row.  A 4-lane group per
+// 1..4-entry row (k_sweep_reg<4>) keeps only 8 rows of a warp in flight and spends
+// shuffles on a handful of items; here a warp has 32 rows' header / stream / entry loads
+// in flight and the row's keys are merged in registers.  Same decision as the group
+// kernels: candidates are the distinct packed keys != own, scored with the same exact
+// integers; argmax by (S desc, label asc) is order-independent.
+template <int L, class WT, bool S64>
+__device__ __forceinline__ void thr_decide(const AggArgs &a, Acc &acc, const RowHdr &h, u64 pr, i64 di, uint32_t dr31,
+                                           const int32_t (&key)[L], const u64 (&wv)[L], const uint32_t (&d31)[L]) {
+  const int32_t own = (int32_t)(uint32_t)pr;
+  Cand best = S64 ? cand_none64() : cand_none();
+  u64 eown = 0;
+#pragma unroll
+  for (int t = 0; t < L; ++t) {
+    if (key[t] == EMPTY) continue;
+    if (key[t] == own) {
+      eown += wv[t];
+      continue;
+    }
+    ++acc.cand;
+    cand_push<S64>(best, a.twoW, di, key[t], wv[t], deg_of(a, d31[t], key_label(key[t])));
+  }
+  const i64 dq = deg_of(a, (uint32_t)(pr >> 32), key_label(own));
+  const i64 dr = deg_of(a, dr31, h.r);
+  sweep_decide<S64>(a, acc, h.r, own, di, dq, dr, best, eown);
+}
+
+template <int L, class WT>
+__global__ void __launch_bounds__(256) k_sweep_thr(AggArgs a) {
+  Acc acc;
+  const u64 pf = l2_policy_first(), pl = l2_policy_last();
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < a.nrows; i += (i64)gridDim.x * 256) {
+    const RowHdr h = a.hdr[i];
+    int32_t col[L];
+    u64 wv[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+      col[t] = EMPTY;
+      wv[t] = 0;
+      if (t < h.len) {
+        if (a.hint & 1) {
+          col[t] = ld_stream(&a.keys[h.beg + t], pf);
+          wv[t] = WT::get(a.w, h.beg + t, pf);
+        } else {
+          col[t] = __ldg(&a.keys[h.beg + t]);
+          wv[t] = WT::get(a.w, h.beg + t);
+        }
+      }
+    }
+    const u64 pr = __ldg(&a.ldeg[h.r]);
+    const i64 di = __ldg(&a.delta[h.r]);
+    const uint32_t dr31 = __ldg(&a.cpk[h.r]) & DEG_SAT;
+    int32_t key[L];
+    uint32_t d31[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+      const u64 p = col[t] != EMPTY ? ld_entry(a, col[t], pl) : 0;
+      key[t] = col[t] != EMPTY ? (int32_t)(uint32_t)p : EMPTY;
+      d31[t] = (uint32_t)(p >> 32);
+    }
+    // merge equal keys into their first occurrence (e_{i->C} per community, Eq. 1)
+#pragma unroll
+    for (int t = 1; t < L; ++t)
+#pragma unroll
+      for (int u = 0; u < t; ++u)
+        if (key[t] != EMPTY && key[u] == key[t]) {
+          wv[u] += wv[t];
+          key[t] = EMPTY;
+        }
+    if (row_s64(a.twoW, di)) thr_decide<L, WT, true>(a, acc, h, pr, di, dr31, key, wv, d31);
+    else thr_decide<L, WT, false>(a, acc, h, pr, di, dr31, key, wv, d31);
+  }
+  acc.flush(a.counters);
+}
+
 // ----------------------------------------------------------------- hub path
 // Rows longer than the largest shared-memory bin (> 4096 entries).  Instead of one
 // global hash table per row (random read-modify-writes over a table far larger than

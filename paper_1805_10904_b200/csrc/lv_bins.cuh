@@ -36,10 +36,19 @@ struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
   std::vector<std::string> names;
   std::vector<cudaEvent_t> t0, t1;
   std::vector<size_t> open;
+  std::vector<cudaEvent_t> pool;  // events are reused across clear() (creation costs host time)
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
   void begin(cudaStream_t s, const std::string &n) {
     if (!on) return;
-    cudaEvent_t a;
-    cudaEventCreate(&a);
+    cudaEvent_t a = get();
     cudaEventRecord(a, s);
     names.push_back(n);
     t0.push_back(a);
@@ -48,22 +57,21 @@ struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
   }
   void end(cudaStream_t s) {
     if (!on || open.empty()) return;
-    cudaEvent_t b;
-    cudaEventCreate(&b);
+    cudaEvent_t b = get();
     cudaEventRecord(b, s);
     t1[open.back()] = b;
     open.pop_back();
   }
   void clear() {
-    for (auto e : t0) cudaEventDestroy(e);
-    for (auto e : t1)
-      if (e) cudaEventDestroy(e);
     t0.clear();
     t1.clear();
     names.clear();
     open.clear();
+    used = 0;
   }
-  ~KTimer() { clear(); }
+  ~KTimer() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
 };
 
 struct Bins {
@@ -308,6 +316,25 @@ void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   // one wins).  LV_REG_PIPE=0 / 2 force plain / pipelined everywhere.
   static const int pipe_env = getenv("LV_REG_PIPE") ? atoi(getenv("LV_REG_PIPE")) : 1;
   const bool pipe = pipe_env == 2 || (pipe_env == 1 && G <= 16);
+  // SWEEP rows of <= LV_THR (default 8) entries: a thread per row (k_sweep_thr; C4 level-0
+  // sweep: <= 8 bin 0.35 -> 0.26 ms, <= 4 bin 0.85 -> 0.80 ms, tools/variants.sh)
+  if constexpr (MODE == M_SWEEP && G <= 8) {
+    static const int thr_env = getenv("LV_THR") ? atoi(getenv("LV_THR")) : 8;
+    if (G <= thr_env) {
+      auto kt = k_sweep_thr<G, WT>;
+      static int occ_t = -1;
+      if (occ_t < 0) {
+        int o = 0;
+        LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kt, 256, 0));
+        occ_t = o > 0 ? o : 1;
+      }
+      const i64 grid_t = std::min<i64>(cdiv(a.nrows, 256), (i64)c.sms * occ_t * 8);
+      if (tm) tm->begin(st, tag);
+      LV_LAUNCH_ON(c, st, kt, (unsigned)grid_t, 256, 0, a);
+      if (tm) tm->end(st);
+      return;
+    }
+  }
   auto kern = (MODE == M_SWEEP && pipe) ? k_sweep_reg<G, BLOCK, WT, NARROW> : k_agg_reg<G, BLOCK, MODE, WT, NARROW>;
   constexpr int GPB = BLOCK / G;
   static int occ = -1;

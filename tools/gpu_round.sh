@@ -10,7 +10,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${TAG}_smoke.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > $O/${TAG}_ncu_bench.log 2>&1
+    --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 0 --e2e-steps 0 --coloring-steps 0 --no-cpu-baseline > $O/${TAG}_ncu_bench.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
     --profile-from-start off -o $O/${TAG}_sweep_full -f \
     env LV_PROFILE_RANGE=1 python tools/profile_sweep.py --workload rmat24 --warm 3 --reps 1 > $O/${TAG}_ncu_full.log 2>&1
