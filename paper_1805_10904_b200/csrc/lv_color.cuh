@@ -34,6 +34,12 @@ __device__ __forceinline__ u64 color_prio(i64 v) {  // MurmurHash3 fmix64 (a bij
 // lower-priority neighbours, which join the next frontier when theirs reaches 0.  Same
 // colouring as the sequential greedy in decreasing-π order; rounds = the longest
 // decreasing-priority path.
+// π of every row, once per colouring (saves the orig[] indirection in every scan)
+__global__ void k_jp_prio(i64 n, const int32_t *__restrict__ orig, u64 *pri) {
+  for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256)
+    pri[v] = color_prio(orig ? orig[v] : v);
+}
+
 // Rows longer than JP_LONG take a CTA each (k_jp_round_long) — a warp per 400k-entry hub
 // row would serialise its round.  Frontier lists: [0] short rows, [1] long rows.
 constexpr i64 JP_LONG = 1024;
@@ -47,17 +53,14 @@ __device__ __forceinline__ void jp_push(const i64 *rp, int32_t u, int32_t *wl_s,
 }
 
 __global__ void __launch_bounds__(256) k_jp_init(i64 n, const i64 *__restrict__ rp, const int32_t *__restrict__ col,
-                                                 const int32_t *__restrict__ orig, int32_t *wait, int32_t *wl_s,
+                                                 const u64 *__restrict__ pri, int32_t *wait, int32_t *wl_s,
                                                  u64 *cnt_s, int32_t *wl_l, u64 *cnt_l) {
   const int lane = threadIdx.x & 31;
   const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 v = (((i64)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; v < n; v += nw) {
-    const u64 pv = color_prio(orig ? orig[v] : v);
+    const u64 pv = pri[v];
     int32_t c = 0;
-    for (i64 k = rp[v] + lane; k < rp[v + 1]; k += 32) {
-      const int32_t u = col[k];
-      c += color_prio(orig ? orig[u] : u) > pv;
-    }
+    for (i64 k = rp[v] + lane; k < rp[v + 1]; k += 32) c += pri[col[k]] > pv;
     c = __reduce_add_sync(0xffffffffu, (uint32_t)c);
     if (lane == 0) {
       wait[v] = c;
@@ -66,10 +69,12 @@ __global__ void __launch_bounds__(256) k_jp_init(i64 n, const i64 *__restrict__ 
   }
 }
 
-// Short rows: a warp each.
+// Short rows: a warp each; 4 entries per lane in flight (the round's critical path is
+// its longest row's chain of dependent loads).
+constexpr int JP_U = 4;
 __global__ void __launch_bounds__(256) k_jp_round(const int32_t *__restrict__ wl_in, const u64 *__restrict__ cnt_in,
                                                   const i64 *__restrict__ rp, const int32_t *__restrict__ col,
-                                                  const int32_t *__restrict__ orig, int32_t *color, int32_t *wait,
+                                                  const u64 *__restrict__ pri, int32_t *color, int32_t *wait,
                                                   int32_t *wl_s, u64 *cnt_s, int32_t *wl_l, u64 *cnt_l) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -77,18 +82,30 @@ __global__ void __launch_bounds__(256) k_jp_round(const int32_t *__restrict__ wl
   const i64 cnt = (i64)*cnt_in;
   for (i64 t = (((i64)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; t < cnt; t += nw) {
     const int32_t v = wl_in[t];
-    const u64 pv = color_prio(orig ? orig[v] : v);
+    const u64 pv = pri[v];
     const i64 b = rp[v], e = rp[v + 1];
     int c = -1;
     for (int base = 0; c < 0; base += 64) {  // colour windows [base, base + 64)
       u64 m = 0;
-      for (i64 k = b + lane; k < e; k += 32) {
-        const int32_t u = col[k];
-        if (color_prio(orig ? orig[u] : u) > pv) {
-          const int32_t cu = __ldcg(&color[u]);  // final: coloured in an earlier round
-          if (cu >= base && cu < base + 64) m |= 1ull << (cu - base);
-        } else if (base == 0 && atomicSub(&wait[u], 1) == 1) {  // u's last higher neighbour
-          jp_push(rp, u, wl_s, cnt_s, wl_l, cnt_l);
+      for (i64 k0 = b; k0 < e; k0 += 32 * JP_U) {
+        int32_t u[JP_U];
+        bool hi[JP_U];
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) {
+          const i64 k = k0 + j * 32 + lane;
+          u[j] = k < e ? col[k] : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) hi[j] = u[j] >= 0 && pri[u[j]] > pv;
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) {
+          if (u[j] < 0) continue;
+          if (hi[j]) {
+            const int32_t cu = __ldcg(&color[u[j]]);  // final: coloured in an earlier round
+            if (cu >= base && cu < base + 64) m |= 1ull << (cu - base);
+          } else if (base == 0 && atomicSub(&wait[u[j]], 1) == 1) {  // u's last higher neighbour
+            jp_push(rp, u[j], wl_s, cnt_s, wl_l, cnt_l);
+          }
         }
       }
       const u64 all = ((u64)__reduce_or_sync(full, (uint32_t)(m >> 32)) << 32) | __reduce_or_sync(full, (uint32_t)m);
@@ -102,7 +119,7 @@ __global__ void __launch_bounds__(256) k_jp_round(const int32_t *__restrict__ wl
 __global__ void __launch_bounds__(JP_CTA) k_jp_round_long(const int32_t *__restrict__ wl_in,
                                                           const u64 *__restrict__ cnt_in, const i64 *__restrict__ rp,
                                                           const int32_t *__restrict__ col,
-                                                          const int32_t *__restrict__ orig, int32_t *color,
+                                                          const u64 *__restrict__ pri, int32_t *color,
                                                           int32_t *wait, int32_t *wl_s, u64 *cnt_s, int32_t *wl_l,
                                                           u64 *cnt_l) {
   __shared__ uint32_t bits[JP_BITS / 32];
@@ -110,20 +127,32 @@ __global__ void __launch_bounds__(JP_CTA) k_jp_round_long(const int32_t *__restr
   const i64 cnt = (i64)*cnt_in;
   for (i64 t = blockIdx.x; t < cnt; t += gridDim.x) {
     const int32_t v = wl_in[t];
-    const u64 pv = color_prio(orig ? orig[v] : v);
+    const u64 pv = pri[v];
     const i64 b = rp[v], e = rp[v + 1];
     int c = -1;
     for (int base = 0; c < 0; base += JP_BITS) {
       for (int i = threadIdx.x; i < JP_BITS / 32; i += JP_CTA) bits[i] = 0;
       if (threadIdx.x == 0) best = INT32_MAX;
       __syncthreads();
-      for (i64 k = b + threadIdx.x; k < e; k += JP_CTA) {
-        const int32_t u = col[k];
-        if (color_prio(orig ? orig[u] : u) > pv) {
-          const int32_t cu = __ldcg(&color[u]) - base;
-          if (cu >= 0 && cu < JP_BITS) atomicOr(&bits[cu >> 5], 1u << (cu & 31));
-        } else if (base == 0 && atomicSub(&wait[u], 1) == 1) {
-          jp_push(rp, u, wl_s, cnt_s, wl_l, cnt_l);
+      for (i64 k0 = b; k0 < e; k0 += (i64)JP_CTA * JP_U) {
+        int32_t u[JP_U];
+        bool hi[JP_U];
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) {
+          const i64 k = k0 + (i64)j * JP_CTA + threadIdx.x;
+          u[j] = k < e ? col[k] : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) hi[j] = u[j] >= 0 && pri[u[j]] > pv;
+#pragma unroll
+        for (int j = 0; j < JP_U; ++j) {
+          if (u[j] < 0) continue;
+          if (hi[j]) {
+            const int32_t cu = __ldcg(&color[u[j]]) - base;
+            if (cu >= 0 && cu < JP_BITS) atomicOr(&bits[cu >> 5], 1u << (cu & 31));
+          } else if (base == 0 && atomicSub(&wait[u[j]], 1) == 1) {
+            jp_push(rp, u[j], wl_s, cnt_s, wl_l, cnt_l);
+          }
         }
       }
       __syncthreads();
@@ -200,16 +229,18 @@ inline int32_t color_graph(Ctx &c, i64 n, const i64 *rp, const int32_t *col, con
   LV_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(u64), c.s));
   const unsigned grid = (unsigned)std::min<i64>(cdiv(n, 8), (i64)c.sms * 8);
   const unsigned grid_l = (unsigned)c.sms * 2;
-  LV_LAUNCH(c, k_jp_init, grid, 256, 0, n, rp, col, orig, wait.p, wl[0][0].p, cnt.p, wl[0][1].p, cnt.p + 1);
+  Buf<u64> pri(c.A, n);
+  LV_LAUNCH(c, k_jp_prio, grid_for(c, n), 256, 0, n, orig, pri.p);
+  LV_LAUNCH(c, k_jp_init, grid, 256, 0, n, rp, col, pri.p, wait.p, wl[0][0].p, cnt.p, wl[0][1].p, cnt.p + 1);
   int32_t rounds = 0, cur = 0;
   for (;;) {
     for (int r = 0; r < ROUNDS_PER_SYNC; ++r) {
       const int nx = cur ^ 1;
       u64 *cs = cnt.p + 2 * nx, *cl = cnt.p + 2 * nx + 1;
       LV_CUDA(cudaMemsetAsync(cs, 0, 2 * sizeof(u64), c.s));
-      LV_LAUNCH(c, k_jp_round_long, grid_l, JP_CTA, 0, wl[cur][1].p, cnt.p + 2 * cur + 1, rp, col, orig, color.p,
+      LV_LAUNCH(c, k_jp_round_long, grid_l, JP_CTA, 0, wl[cur][1].p, cnt.p + 2 * cur + 1, rp, col, pri.p, color.p,
                 wait.p, wl[nx][0].p, cs, wl[nx][1].p, cl);
-      LV_LAUNCH(c, k_jp_round, grid, 256, 0, wl[cur][0].p, cnt.p + 2 * cur, rp, col, orig, color.p, wait.p,
+      LV_LAUNCH(c, k_jp_round, grid, 256, 0, wl[cur][0].p, cnt.p + 2 * cur, rp, col, pri.p, color.p, wait.p,
                 wl[nx][0].p, cs, wl[nx][1].p, cl);
       cur = nx;
       ++rounds;
