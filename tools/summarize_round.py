@@ -57,7 +57,7 @@ if os.path.exists(lf):
         tot[name] += v
         cnt[name] += 1
     T = sum(tot.values())
-    out.append(f"## Launches of one bench step (`{tag}_launches.csv`: ncu --metrics gpu__time_duration.sum "
+    out.append(f"## Launches of `bench.py --steps 1 --warmup 0` (the timed step + the profiled step; `{tag}_launches.csv`: ncu --metrics gpu__time_duration.sum "
                f"--clock-control none; cold-cache, serialised)\n")
     out.append(f"{len(rows)} launches, total kernel time {T:.1f} ms.\n")
     out.append("| share | total ms | launches | kernel |\n|---|---|---|---|")
