@@ -312,8 +312,8 @@ def main():
             a[2] += k["launches"]
     sweep_pass = agg.pop("sweep_pass", None)  # whole-pass wall time (all bins, concurrent)
     top = max(agg, key=lambda k: agg[k][0]) if agg else None
-    t_ms, t_bytes, t_launch = agg[top] if agg else (float("nan"), float("nan"), 1.0)
-    achieved = t_bytes / (t_ms / 1e3) / 1e9
+    t_ms, t_bytes, t_launch = agg[top] if agg else (None, None, None)
+    achieved = t_bytes / (t_ms / 1e3) / 1e9 if agg else None
     sweep_ms = sweep_pass[0] if sweep_pass else None
     traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -327,12 +327,15 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note, "kernel": top,
-                "kernel_ms_per_launch": t_ms / t_launch, "alg_bytes_per_launch": t_bytes / t_launch,
-                "kernel_share_of_step": t_ms / prof_ms, "profiled_step_ms": prof_ms, "peak_source": pk["source"],
+                "frac": achieved / pk["hbm_gbs"] if agg else None, "traffic": traffic, "traffic_note": traffic_note,
+                "kernel": top, "kernel_ms_per_launch": t_ms / t_launch if agg else None,
+                "alg_bytes_per_launch": t_bytes / t_launch if agg else None,
+                "kernel_share_of_step": t_ms / prof_ms if agg else None, "profiled_step_ms": prof_ms,
+                "peak_source": pk["source"],
                 "note": "per-kernel times: CUDA events on each kernel's launching stream during one profiled step "
                         "run right after the timed steps (same workload; events cost host time per launch); "
-                        "achieved = algorithmic bytes (DESIGN.md §6) / time, averaged over all levels' launches"}
+                        "achieved = algorithmic bytes (DESIGN.md §6) / time, averaged over all levels' launches"
+                        + ("" if agg else "; the sweep-sharded mode (N > 1) has no per-kernel timer: see the N = 1 line")}
     sweep_roof = None
     if sweep_pass:
         sp_ms, sp_bytes, sp_n = sweep_pass
