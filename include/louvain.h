@@ -102,6 +102,9 @@ typedef struct {
                                 Not available in the sweep-sharded mode (LV_EINVAL).       */
     int32_t color_classes;   /* D29: colours >= color_classes-1 share the last class
                                 (swept synchronously); 0 = one class per colour; default 32 */
+    int64_t color_cap_min_n; /* D29: the class cap applies only to level graphs of more than
+                                this many vertices (small dense levels keep every colour, so
+                                no synchronous class oscillates there); default 65536     */
 } louvain_config;
 
 /* Fill `cfg` with the defaults above. */

@@ -60,6 +60,7 @@ class _Config(C.Structure):
         ("theta_schedule_len", C.c_int32),
         ("coloring", C.c_int32),
         ("color_classes", C.c_int32),
+        ("color_cap_min_n", C.c_int64),
     ]
 
 
@@ -269,7 +270,7 @@ def color_priority(v: int) -> int:
 
 def run(graph: Graph, theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64,
         stop_rule=0, merge_isolated=True, theta_schedule=None, coloring=False,
-        color_classes=32) -> Result:
+        color_classes=32, color_cap_min_n=65536) -> Result:
     """Algorithm 2 around Algorithm 1 with the DESIGN.md readings."""
     cfg = _Config()
     _L().og_config_default(C.byref(cfg))
@@ -278,6 +279,7 @@ def run(graph: Graph, theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64,
     cfg.stop_rule, cfg.merge_isolated = int(stop_rule), int(bool(merge_isolated))
     cfg.coloring = int(bool(coloring))
     cfg.color_classes = int(color_classes)
+    cfg.color_cap_min_n = int(color_cap_min_n)
     sched = None
     if theta_schedule:
         sched = (C.c_double * len(theta_schedule))(*theta_schedule)

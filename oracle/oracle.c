@@ -45,7 +45,8 @@ void og_config_default(og_config *c) {
     c->theta_schedule = NULL; /* D21 */
     c->theta_schedule_len = 0;
     c->coloring = 0;          /* D29: off (the paper's pure Jacobi sweeps) */
-    c->color_classes = 32;    /* D29: colours >= 31 share the last class */
+    c->color_classes = 32;    /* D29: colours >= 31 share the last class ... */
+    c->color_cap_min_n = 65536; /* ... on level graphs of more than 65536 vertices */
 }
 
 /* ------------------------------------------------------- graph construction */
@@ -482,7 +483,7 @@ static int one_level(const og_graph *g, const og_config *cfg, double theta, int3
     if (cfg->coloring) {                                  /* D29: colour the level graph */
         color = (int32_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
         if (!color || (K = og_color(g, color)) < 0) { free(color); free(next); free(deg); return OG_ENOMEM; }
-        if (cfg->color_classes > 0 && K > cfg->color_classes) {   /* D29 class cap */
+        if (cfg->color_classes > 0 && K > cfg->color_classes && n > cfg->color_cap_min_n) {   /* D29 cap */
             K = cfg->color_classes;
             for (int64_t i = 0; i < n; ++i) if (color[i] > K - 1) color[i] = K - 1;
         }

@@ -53,6 +53,7 @@ typedef struct {
     int32_t theta_schedule_len;
     int32_t coloring;         /* F2 / D29: 1 = sweep colour classes in turn         */
     int32_t color_classes;    /* D29: classes = min(colour, color_classes-1); 0 = all */
+    int64_t color_cap_min_n;  /* D29: the cap applies to level graphs of > this many vertices */
 } og_config;
 
 /* error codes (0 = ok) */

@@ -61,6 +61,7 @@ class Config(C.Structure):
         ("profile", C.c_int32),
         ("coloring", C.c_int32),
         ("color_classes", C.c_int32),
+        ("color_cap_min_n", C.c_int64),
     ]
 
 

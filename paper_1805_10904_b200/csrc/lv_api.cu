@@ -514,7 +514,8 @@ struct ColorPlan {
   bool capped = false;  // the last class holds every colour >= cap-1 (not independent)
 };
 
-ColorPlan make_color_plan(louvain_ctx *h, const DGraph &g, const int32_t *orig) {
+// level_n: vertices of the level graph (before compaction) — the cap's size test (D29)
+ColorPlan make_color_plan(louvain_ctx *h, const DGraph &g, const int32_t *orig, i64 level_n) {
   Ctx &c = h->c;
   ColorPlan CP;
   Buf<int32_t> color;
@@ -523,7 +524,7 @@ ColorPlan make_color_plan(louvain_ctx *h, const DGraph &g, const int32_t *orig) 
   const double t1 = now_ms();
   int32_t K = CP.colors;
   const int32_t cap = h->cfg.color_classes;
-  if (cap > 0 && K > cap) {
+  if (cap > 0 && K > cap && level_n > h->cfg.color_cap_min_n) {
     LV_LAUNCH(c, k_cap_classes, grid_for(c, g.n), 256, 0, g.n, color.p, cap);
     K = cap;
     CP.capped = true;
@@ -646,7 +647,7 @@ void run_impl(louvain_ctx *h) {
         orig.alloc(c.A, gs.n);
         LV_LAUNCH(c, k_gather_i32, grid_for(c, gs.n), 256, 0, gs.n, cp.rk.p, cp.inv.p, orig.p);
       }
-      CP = make_color_plan(h, gs, compacted ? orig.p : nullptr);
+      CP = make_color_plan(h, gs, compacted ? orig.p : nullptr, g->n);
       rec->colors = CP.colors;
       rec->color_rounds = CP.rounds;
     }
@@ -763,6 +764,7 @@ louvain_status louvain_config_default(louvain_config *cfg) {
   cfg->world = 1;
   cfg->coloring = 0;
   cfg->color_classes = 32;
+  cfg->color_cap_min_n = 65536;
   return LV_OK;
 }
 

@@ -40,8 +40,9 @@ def test_coloring_parity(name):
 def test_colored_full_run_parity(name, cap):
     r = GRAPHS[name]()
     og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
-    want = oracle.run(og, coloring=True, color_classes=cap)
-    with Louvain(r.n, r.src, r.dst, r.w, coloring=True, color_classes=cap) as g:
+    # color_cap_min_n=0: cap every level, so the synchronous last class (k_delta_i2) runs
+    want = oracle.run(og, coloring=True, color_classes=cap, color_cap_min_n=0)
+    with Louvain(r.n, r.src, r.dst, r.w, coloring=True, color_classes=cap, color_cap_min_n=0) as g:
         g.run()
         assert g.num_levels == len(want.levels)
         for l in range(g.num_levels):
@@ -51,6 +52,16 @@ def test_colored_full_run_parity(name, cap):
         assert np.array_equal(g.partition(-1), want.final)
         assert g.modularity(-1) == want.final_q
         assert g.level_colors(0)[0] >= 1
+
+
+def test_colored_default_cap_threshold():
+    """Default D29 cap: levels of <= 65536 vertices keep one class per colour."""
+    r = inputs.sbm(20_000, 20, 32, 0.3, seed=2)
+    want = oracle.run(oracle.Graph.from_edges(r.n, r.src, r.dst), coloring=True)
+    with Louvain(r.n, r.src, r.dst, coloring=True) as g:
+        g.run()
+        assert [g.level_stats(l)[0] for l in range(g.num_levels)] == want.sweeps
+        assert np.array_equal(g.partition(-1), want.final) and g.modularity(-1) == want.final_q
 
 
 @pytest.mark.parametrize("stop_rule", [0, 1])
