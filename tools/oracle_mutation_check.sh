@@ -4,12 +4,12 @@
 # Run from the repo root:  bash tools/oracle_mutation_check.sh
 set -u
 cd "$(dirname "$0")/.."
-mut() {
+mut() {  # mut SED NAME [TESTFILE]
   cp oracle/oracle.c /tmp/oracle.c.bak
   sed -i "$1" oracle/oracle.c
   if cmp -s oracle/oracle.c /tmp/oracle.c.bak; then echo "[$2] SED DID NOT APPLY"; return; fi
   rm -f oracle/liboracle.so
-  r=$(timeout 600 python -m pytest tests/test_oracle_pins.py -x -q 2>&1 | tail -1)
+  r=$(timeout 600 python -m pytest "${3:-tests/test_oracle_pins.py}" -x -q 2>&1 | tail -1)
   echo "[$2] $r"
   cp /tmp/oracle.c.bak oracle/oracle.c
   rm -f oracle/liboracle.so
@@ -28,3 +28,15 @@ mut 's/i128 S = twoW \* st->e\[c\] - di \* (i128)st->deg\[c\];/i128 S = twoW * s
 mut 's/for (s = 1; s <= cfg->max_sweeps; ++s) {/for (s = 1; s <= cfg->max_sweeps - 1; ++s) {/' "cap off by one (D12)"
 mut 's/if (l == 0 || !(Ql - mod_curr < cfg->big_theta))/if (!(Ql - mod_curr < cfg->big_theta))/' "level 0 not forced (Alg.2)"
 mut 's/return neg ? -d : d;/return d;/' "d128 sign lost (D22)"
+# real weights (F1, reading D28) -> tests/test_oracle_real.py
+R=tests/test_oracle_real.py
+mut 's/static double fixed_of(double w, int32_t s) { return rint(ldexp(w, s)); }/static double fixed_of(double w, int32_t s) { return round(ldexp(w, s)); }/' "half away from zero (D28 rint)" $R
+mut 's/if (og_fixed_sum(m, w, mid) <= lim) lo = mid; else hi = mid;/if (og_fixed_sum(m, w, mid) < lim \/ 2) lo = mid; else hi = mid;/' "scale one bit short (D28 largest s)" $R
+mut 's/const int64_t lim = (int64_t)1 << 52;/const int64_t lim = (int64_t)1 << 53;/' "2W budget instead of W (D28)" $R
+mut 's/int32_t lo = -1100, hi = 1100; /int32_t lo = -60, hi = 60; /' "scale search range too narrow (D28)" $R
+# colouring heuristic (F2, reading D29) -> tests/test_oracle_coloring.py
+Cf=tests/test_oracle_coloring.py
+mut 's/return x < y ? 1 : x > y ? -1 : 0;/return x < y ? -1 : x > y ? 1 : 0;/' "ascending priority order (D29)" $Cf
+mut 's/k ^= k >> 33; k \*= 0xff51afd7ed558ccdull;/k ^= k >> 31; k *= 0xff51afd7ed558ccdull;/' "wrong fmix64 shift (D29)" $Cf
+mut 's/while (used\[c\]) ++c;                                              \/\* smallest free \*\//c = 0; while (used[c]) c += 2;/' "not the smallest free colour (D29)" $Cf
+mut 's/memcpy(cur, labels_out, (size_t)n \* sizeof(int32_t));   \/\* commit class c \*\//(void)0;/' "classes see the sweep-start state (Jacobi, D29)" $Cf
