@@ -558,7 +558,16 @@ int32_t one_level_colored(louvain_ctx *h, const DGraph &g, const ColorPlan &CP, 
   bool first = true;
   double Qp = 0.0;
   int32_t s;
-  for (s = 1; s <= cfg.max_sweeps; ++s) {
+  // The class sequence of a sweep is the same launches every sweep (only the state
+  // buffers alternate), so from sweep 2 on it replays as a CUDA graph — one per parity of
+  // the starting buffer — instead of K classes x ~15 launches (launch-bound on small
+  // levels).  Sweep 1 runs eagerly (first-use kernel attributes).  LV_NO_GRAPH=1: eager.
+  static const bool no_graph = getenv("LV_NO_GRAPH") != nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  i64 glaunch[2] = {0, 0};  // kernels per graph (counted into c.launches per replay)
+  int nact = 0;
+  for (size_t k = 0; k < K; ++k) nact += CP.cls[k]->active() > 0;
+  auto enqueue_sweep = [&]() {
     LV_CUDA(cudaMemsetAsync(ctr.p, 0, (K * SLOT + 4) * sizeof(u64), c.s));
     for (size_t k = 0; k < K; ++k) {
       const Bins &B = *CP.cls[k];
@@ -569,8 +578,54 @@ int32_t one_level_colored(louvain_ctx *h, const DGraph &g, const ColorPlan &CP, 
                   (const void *)g.w.p, g.wt, st.lab[st.cur].p, st.lab[st.cur ^ 1].p, ctr.p + K * SLOT);
       commit(h, g, st);
     }
-    h->edge_visits += g.nnz;
     LV_LAUNCH(c, k_sumsq_u128<DegArr>, grid_for(c, g.n), 256, 0, DegArr{st.deg[st.cur].p}, g.n, ctr.p + K * SLOT + 1);
+  };
+  struct GraphGuard {
+    cudaGraphExec_t *e;
+    ~GraphGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaGraphExecDestroy(e[i]);
+    }
+  } guard{gexec};
+  for (s = 1; s <= cfg.max_sweeps; ++s) {
+    const int c0 = st.cur;
+    if (s == 1 || no_graph || c.concurrent) {
+      enqueue_sweep();
+    } else {
+      bool fresh = false;
+      if (!gexec[c0]) {
+        cudaGraph_t gr = nullptr;
+        const i64 l0 = c.launches;
+        LV_CUDA(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+        c.capturing = true;
+        try {
+          enqueue_sweep();
+        } catch (...) {
+          c.capturing = false;
+          cudaStreamEndCapture(c.s, &gr);
+          if (gr) cudaGraphDestroy(gr);
+          throw;
+        }
+        c.capturing = false;
+        LV_CUDA(cudaStreamEndCapture(c.s, &gr));
+        const cudaError_t ie = cudaGraphInstantiate(&gexec[c0], gr, 0);
+        cudaGraphDestroy(gr);
+        LV_CUDA(ie);
+        glaunch[c0] = c.launches - l0;  // counted once by the capture itself
+        fresh = true;
+      }
+      if (!fresh) c.launches += glaunch[c0];
+      st.cur = c0 ^ (nact & 1);  // the flips the sweep's K commits make
+      LV_CUDA(cudaGraphLaunch(gexec[c0], c.s));
+      for (size_t k = 0; k < K; ++k)  // the hub-bucket check the eager passes make
+        if (CP.cls[k]->nhub) {
+          int ovf = 0;
+          LV_CUDA(cudaMemcpyAsync(&ovf, CP.cls[k]->overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+          LV_CUDA(cudaStreamSynchronize(c.s));
+          LV_REQUIRE(ovf == 0, LV_ECUDA, "hub bucket overflow (a hash bucket exceeded its table)");
+        }
+    }
+    h->edge_visits += g.nnz;
     LV_CUDA(cudaMemcpyAsync(hc.data(), ctr.p, hc.size() * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
     // independent classes: ΔI2 = 2(Σ e_best − Σ e_own) over the movers, where the kernels

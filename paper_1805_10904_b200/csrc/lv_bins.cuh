@@ -476,7 +476,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
       LV_CUDA(cudaStreamWaitEvent(c.s, c.join_ev[i], 0));
     }
   }
-  if (B.nhub) {  // a bucket beyond its distinct-key capacity would have been dropped
+  if (B.nhub && !c.capturing) {  // a bucket beyond its distinct-key capacity would have been dropped
     int ovf = 0;
     LV_CUDA(cudaMemcpyAsync(&ovf, B.overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));

@@ -144,6 +144,7 @@ struct Ctx {
   cudaStream_t side[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fork_ev = nullptr, join_ev[NSIDE] = {nullptr, nullptr, nullptr, nullptr};
   bool concurrent = false;
+  bool capturing = false;  // a CUDA-graph capture is open on s: no host syncs may be issued
   void init_side() {
     for (int i = 0; i < NSIDE; ++i) {
       if (cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking) != cudaSuccess) return;
