@@ -529,10 +529,7 @@ ColorPlan make_color_plan(louvain_ctx *h, const DGraph &g, const int32_t *orig, 
     K = cap;
     CP.capped = true;
   }
-  for (int32_t k = 0; k < K; ++k) {
-    CP.cls.push_back(std::make_unique<Bins>());
-    build_bins(c, g.row_ptr.p, g.n, g.n, *CP.cls.back(), 0, -1, false, color.p, k);
-  }
+  build_class_bins(c, g.row_ptr.p, g.n, color.p, K, CP.cls);
   LV_CUDA(cudaStreamSynchronize(c.s));
   if (getenv("LV_COLOR_TRACE"))
     fprintf(stderr, "colour plan: n=%lld colours=%d rounds=%d colour %.1f ms, class bins %.1f ms\n", (long long)g.n,

@@ -178,6 +178,8 @@ inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
 // most `universe` distinct keys per row.
 // Only rows in [lo, hi) are binned (hi < 0: all rows).  rows_only: just B.rows / B.off
 // (the per-bin row lists, ascending within a bin), no headers, edge counts or hub tables.
+inline void finish_bins(Ctx &c, const i64 *ptr, i64 universe, Bins &B, const std::vector<i64> &cnt, const i64 *edges);
+
 inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B, i64 lo = 0, i64 hi = -1,
                        bool rows_only = false, const int32_t *cls = nullptr, int32_t ck = 0) {
   B.nrows = nrows;
@@ -200,10 +202,19 @@ inline void build_bins(Ctx &c, const i64 *ptr, i64 nrows, i64 universe, Bins &B,
     LV_LAUNCH(c, k_bin_scatter, grid_for(c, nrows), 256, 0, nrows, ids.p, b, pos.p, B.rows.p + B.off[b]);
   }
   if (rows_only) return;
+  finish_bins(c, ptr, universe, B, cnt, nullptr);
+}
+
+// Row headers, per-bin edge counts (given, or summed here) and the hub path's chunk /
+// bucket tables of bins whose rows (B.rows, B.off) are already grouped.
+inline void finish_bins(Ctx &c, const i64 *ptr, i64 universe, Bins &B, const std::vector<i64> &cnt,
+                        const i64 *edges) {
   B.hdr.alloc(c.A, B.off[NBIN] > 0 ? B.off[NBIN] : 1);
   if (B.off[NSMEM] > 0)
     LV_LAUNCH(c, k_fill_hdr, grid_for(c, B.off[NSMEM]), 256, 0, B.off[NSMEM], B.rows.p, ptr, B.hdr.p);
-  {
+  if (edges) {
+    for (int b = 0; b < NBIN; ++b) B.edges[b] = edges[b];
+  } else {
     Buf<u64> es(c.A, NBIN);
     LV_CUDA(cudaMemsetAsync(es.p, 0, NBIN * sizeof(u64), c.s));
     for (int b = 0; b < NBIN; ++b)

@@ -214,6 +214,72 @@ struct ColorArr {
   __device__ __forceinline__ u64 operator()(i64 i) const { return (u64)(i64)c[i]; }
 };
 
+// Degree bins of every colour class at once: one counting pass keyed by
+// (class, bin), one scatter, then per class a slice copy + headers (+ hub tables) —
+// instead of K full build_bins passes (9 scans each), which dominated small dense levels
+// with hundreds of classes.  Row order within a (class, bin) follows the scatter's atomics:
+// every consumer's result is order-independent (exact sums, total-order argmax).
+__global__ void k_cls_count(i64 n, const i64 *__restrict__ rp, const int32_t *__restrict__ cls, uint32_t *cnt,
+                            u64 *edges) {
+  for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256) {
+    const i64 d = rp[r + 1] - rp[r];
+    const int b = bin_of(d);
+    if (b == 255) continue;
+    const i64 key = (i64)cls[r] * NBIN + b;
+    atomicAdd(&cnt[key], 1u);
+    atomicAdd((unsigned long long *)&edges[key], (unsigned long long)d);
+  }
+}
+
+__global__ void k_cls_scatter(i64 n, const i64 *__restrict__ rp, const int32_t *__restrict__ cls,
+                              const i64 *__restrict__ off, uint32_t *cur, int32_t *rows) {
+  for (i64 r = (i64)blockIdx.x * 256 + threadIdx.x; r < n; r += (i64)gridDim.x * 256) {
+    const int b = bin_of(rp[r + 1] - rp[r]);
+    if (b == 255) continue;
+    const i64 key = (i64)cls[r] * NBIN + b;
+    rows[off[key] + atomicAdd(&cur[key], 1u)] = (int32_t)r;
+  }
+}
+
+inline void build_class_bins(Ctx &c, const i64 *rp, i64 n, const int32_t *cls, int32_t K,
+                             std::vector<std::unique_ptr<Bins>> &out) {
+  const size_t nk = (size_t)K * NBIN;
+  Buf<uint32_t> cnt(c.A, 2 * nk);
+  Buf<u64> ed(c.A, nk);
+  LV_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * nk * sizeof(uint32_t), c.s));
+  LV_CUDA(cudaMemsetAsync(ed.p, 0, nk * sizeof(u64), c.s));
+  LV_LAUNCH(c, k_cls_count, grid_for(c, n), 256, 0, n, rp, cls, cnt.p, ed.p);
+  std::vector<uint32_t> hc(nk);
+  std::vector<u64> he(nk);
+  LV_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, nk * sizeof(uint32_t), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaMemcpyAsync(he.data(), ed.p, nk * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  std::vector<i64> off(nk + 1, 0);
+  for (size_t k = 0; k < nk; ++k) off[k + 1] = off[k] + hc[k];
+  Buf<i64> doff(c.A, nk + 1);
+  Buf<int32_t> rows(c.A, off[nk] > 0 ? off[nk] : 1);
+  LV_CUDA(cudaMemcpyAsync(doff.p, off.data(), (nk + 1) * sizeof(i64), cudaMemcpyHostToDevice, c.s));
+  LV_LAUNCH(c, k_cls_scatter, grid_for(c, n), 256, 0, n, rp, cls, doff.p, cnt.p + nk, rows.p);
+  for (int32_t k = 0; k < K; ++k) {
+    auto B = std::make_unique<Bins>();
+    B->nrows = n;
+    std::vector<i64> cb(NBIN);
+    i64 eb[NBIN];
+    for (int b = 0; b < NBIN; ++b) {
+      cb[b] = hc[(size_t)k * NBIN + b];
+      eb[b] = (i64)he[(size_t)k * NBIN + b];
+      B->off[b + 1] = B->off[b] + cb[b];
+    }
+    const i64 tot = B->off[NBIN];
+    B->rows.alloc(c.A, tot > 0 ? tot : 1);
+    if (tot > 0)
+      LV_CUDA(cudaMemcpyAsync(B->rows.p, rows.p + off[(size_t)k * NBIN], tot * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, c.s));
+    finish_bins(c, rp, n, *B, cb, eb);
+    out.push_back(std::move(B));
+  }
+}
+
 // Colour the n rows of (rp, col); returns the number of colours K.  ROUNDS_PER_SYNC
 // rounds are queued between host checks of the frontier size (a round on an empty
 // frontier is a no-op).
