@@ -11,9 +11,10 @@
  * paper where it is silent or garbled are D1..D27 in DESIGN.md §3; the library and the
  * CPU oracle (oracle/, test-only) implement the same readings independently.
  *
- * Arithmetic (reading D22): integer weights only; all aggregates are exact 64-bit
- * integers and move scores exact 128-bit integers, so partitions are a mathematical
- * function of the input (independent of thread count, schedule and GPU count).
+ * Arithmetic (reading D22): all aggregates are exact 64-bit integers and move scores
+ * exact 128-bit integers, so partitions are a mathematical function of the input
+ * (independent of thread count, schedule and GPU count).  Real (float) weights are mapped
+ * to exact fixed point first (reading D28, louvain_weight_scale).
  *
  * Conventions for every function:
  *  - Return value: LV_OK (0) or an error code; nothing throws across the ABI.  After an
