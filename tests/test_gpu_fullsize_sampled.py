@@ -1,5 +1,6 @@
 """Full-size sampled parity: the first local-move sweep of C4 (R-MAT scale 24, the bench
-workload) on the GPU against the oracle, vertex by vertex.
+workload) and of C3 (the 5M-vertex co-occurrence graph) on the GPU against the oracle,
+vertex by vertex.
 
 The oracle cannot build the whole 520M-entry CSR in seconds, but a sweep-1 decision
 (every community a singleton) only depends on W, δ_i, the weights w_ij to i's
@@ -59,7 +60,8 @@ def _standin_decision(i, src, dst, w, delta, W):
 
 
 def _delta_W(r):
-    w = r.w.astype(np.int64)
+    # unweighted records (C2, C3) carry weight 1 each; duplicates are summed (reading D25)
+    w = np.ones(len(r.src), np.int64) if r.w is None else r.w.astype(np.int64)
     delta = np.bincount(r.src, weights=w, minlength=r.n).astype(np.int64)
     delta += np.bincount(r.dst, weights=w, minlength=r.n).astype(np.int64)
     return w, delta, int(w.sum())
@@ -83,15 +85,31 @@ def test_standin_reproduces_full_graph_decisions():
     assert n_ok > 500
 
 
-@pytest.mark.gpu
-def test_c4_sweep1_sampled_decisions():
-    r = inputs.rmat(24, 16, seed=4)
+def test_standin_reproduces_full_graph_decisions_cooc():
+    """The same CPU check on a small C3-shaped co-occurrence graph: unweighted records with
+    many duplicates (weights by summation, reading D25)."""
+    r = inputs.cooc(topics=40, topic_size=500, docs=60_000, seed=3)
+    w, delta, W = _delta_W(r)
+    og = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    assert np.array_equal(og.arrays()["delta"], delta) and og.W == W
+    full = og.decide(np.arange(r.n, dtype=np.int32), range(r.n))
+    rows = np.bincount(r.src, minlength=r.n) + np.bincount(r.dst, minlength=r.n)
+    n_ok = 0
+    for i in np.nonzero(rows > 0)[0][::7]:
+        d = _standin_decision(int(i), r.src, r.dst, w, delta, W)
+        if d is not None:
+            assert d == full[i], i
+            n_ok += 1
+    assert n_ok > 500
+
+
+def _sampled_sweep1(r, bins, min_checked):
     src, dst = r.src, r.dst
     w, delta, W = _delta_W(r)  # δ (reading D2: a loop adds 2ω) and W (D3) from the records
     rows = np.bincount(src, minlength=r.n) + np.bincount(dst, minlength=r.n)  # incident records
     rng = np.random.default_rng(7)
     samples = []
-    for lo, hi, k in ((1, 4, 6), (5, 32, 6), (33, 512, 6), (513, 4096, 5), (4097, 20000, 4), (20001, 10**9, 3)):
+    for lo, hi, k in bins:
         cand = np.nonzero((rows >= lo) & (rows <= hi))[0]
         samples += [int(x) for x in rng.choice(cand, min(k, len(cand)), replace=False)]
     with Louvain(r.n, r.src, r.dst, r.w) as gl:
@@ -105,5 +123,21 @@ def test_c4_sweep1_sampled_decisions():
             continue
         assert got[i] == want, (i, int(rows[i]), int(got[i]), want)
         checked += 1
-    assert checked >= 25
+    assert checked >= min_checked
     assert moved > 0
+
+
+@pytest.mark.gpu
+def test_c4_sweep1_sampled_decisions():
+    _sampled_sweep1(inputs.rmat(24, 16, seed=4),
+                    ((1, 4, 6), (5, 32, 6), (33, 512, 6), (513, 4096, 5), (4097, 20000, 4),
+                     (20001, 10**9, 3)), 25)
+
+
+@pytest.mark.gpu
+def test_c3_sweep1_sampled_decisions():
+    """C3 at full size (5M vertices, 285M co-occurrence records, unweighted with
+    duplicates): sweep-1 decisions of 30 vertices across the degree bins (rows up to
+    ~20000 entries; C3 has no hub rows beyond that) against the oracle's stand-ins."""
+    _sampled_sweep1(inputs.make("cooc"),
+                    ((1, 4, 6), (5, 32, 6), (33, 512, 6), (513, 4096, 6), (4097, 10**9, 6)), 25)
