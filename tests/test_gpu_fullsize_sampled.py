@@ -116,9 +116,13 @@ def _sampled_sweep1(r, bins, min_checked):
         csr = gl.csr()
         assert csr["W"] == W and np.array_equal(csr["delta"], delta)
         got, moved, _, _ = gl.sweep(np.arange(r.n, dtype=np.int32))
+    # one pass over the records keeps those incident to a sample (all a stand-in reads)
+    S = np.array(samples, dtype=src.dtype)
+    keep = np.isin(src, S) | np.isin(dst, S)
+    ks, kd, kw = src[keep], dst[keep], w[keep]
     checked = 0
     for i in samples:
-        want = _standin_decision(i, src, dst, w, delta, W)
+        want = _standin_decision(i, ks, kd, kw, delta, W)
         if want is None:
             continue
         assert got[i] == want, (i, int(rows[i]), int(got[i]), want)
@@ -141,3 +145,17 @@ def test_c3_sweep1_sampled_decisions():
     ~20000 entries; C3 has no hub rows beyond that) against the oracle's stand-ins."""
     _sampled_sweep1(inputs.make("cooc"),
                     ((1, 4, 6), (5, 32, 6), (33, 512, 6), (513, 4096, 6), (4097, 10**9, 6)), 25)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_c5_sweep1_sampled_decisions():
+    """C5 on one B200 (R-MAT scale 27: 134M vertices, 2.1G records): sweep-1 decisions of
+    30 vertices across all degree bins, hubs included, against the oracle's stand-ins.
+    Needs ~40 GB of host memory for the records and their degree counts."""
+    psutil = pytest.importorskip("psutil")
+    if psutil.virtual_memory().available < 96 << 30:
+        pytest.skip("C5 records need more host memory than this machine has free")
+    _sampled_sweep1(inputs.make("rmat27"),
+                    ((1, 4, 6), (5, 32, 6), (33, 512, 6), (513, 4096, 5), (4097, 20000, 4),
+                     (20001, 10**9, 3)), 25)
