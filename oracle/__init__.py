@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
-GCC_FLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+GCC_FLAGS = ["-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
 
 
 def build(force: bool = False) -> str:
@@ -121,6 +121,8 @@ def _L():
         lib.og_result_edge_visits.argtypes = [P]
         lib.og_result_edge_visits.restype = i64
         lib.og_config_default.argtypes = [C.POINTER(_Config)]
+        lib.og_set_threads.argtypes = [i32]
+        lib.og_get_threads.restype = i32
         _lib = lib
     return _lib
 
@@ -131,6 +133,16 @@ def _ptr(a: np.ndarray | None):
 
 class OracleError(RuntimeError):
     pass
+
+
+def set_threads(t: int) -> None:
+    """OpenMP threads of the oracle's schedule-independent loops (1 = single-threaded).
+    Results are bit-identical for any count (Jacobi sweeps, exact integer sums)."""
+    _L().og_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(_L().og_get_threads())
 
 
 class Graph:

@@ -1,23 +1,39 @@
 /*
- * oracle.c — plain, slow, single-threaded CPU oracle (TEST INFRASTRUCTURE ONLY).
+ * oracle.c — plain, slow CPU oracle (TEST INFRASTRUCTURE ONLY).
  *
  * Follows Forster, arXiv 1805.10904 (/root/reference/PAPER.md, cited "P:Lnn") step by
- * step, with the readings D1..D27 of DESIGN.md §3 wherever the paper is silent, garbled
+ * step, with the readings D1..D29 of DESIGN.md §3 wherever the paper is silent, garbled
  * or inconsistent.  No blocking, fusion or reordering: each function is the paper's
  * definition or algorithm written out.  Library primitives used as steps: qsort.
+ *
+ * Threads (OpenMP: "optionally OpenMP over the scoring loop, which is
+ * still bit-identical under Jacobi").  Only loops whose result cannot depend on the
+ * schedule are parallel:
+ *   - the Jacobi vertex loop of a sweep (every decision reads only the snapshot; each
+ *     thread has its own Eq. 1 scratch),
+ *   - the exact integer sums of Eq. 3 (int64 / int128 addition is associative),
+ *   - the per-row sort of the CSR build and of graph rebuilding (rows are disjoint).
+ * og_set_threads(1) gives the single-threaded oracle; tests/test_oracle_pins.py checks
+ * that 1 and several threads agree bit for bit.
+ *
+ * Sorting by (source, target) (P:L271 sort_by_key) is done as a counting sort
+ * on the source (bucket each record into its row) followed by a qsort of each row on
+ * the target — the same order as one global sort on the pair.
  *
  * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline, --impl reference)
  * may load this file's library.  It shares nothing with paper_1805_10904_b200/.
  *
  * Parity pins: see tests/test_oracle_*.py (Eq. 3 brute force + networkx, gain
  * consistency vs Eq. 3 differences, exhaustive optimum bound, ring of cliques,
- * karate band, SPEC examples, Theorem 1 invariant, weight conservation).
- * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC.
+ * karate band and exact values, SPEC examples, Theorem 1 invariant, weight
+ * conservation, thread-count invariance).
+ * Build: gcc -O2 -std=c11 -fopenmp -ffp-contract=off -fno-fast-math -shared -fPIC.
  */
 #include "oracle.h"
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <omp.h>
 
 typedef __int128 i128;
 
@@ -51,26 +67,24 @@ void og_config_default(og_config *c) {
 
 /* ------------------------------------------------------- graph construction */
 
-typedef struct { int32_t u, v; int64_t w; } rec_t;
+void og_set_threads(int32_t t) { omp_set_num_threads(t > 0 ? t : 1); }
+int32_t og_get_threads(void) { return (int32_t)omp_get_max_threads(); }
 
-static int rec_cmp(const void *a, const void *b) {
-    const rec_t *x = (const rec_t *)a, *y = (const rec_t *)b;
-    if (x->u != y->u) return x->u < y->u ? -1 : 1;
-    if (x->v != y->v) return x->v < y->v ? -1 : 1;
-    return 0;
+typedef struct { int32_t v; int64_t w; } ent_t;
+
+static int ent_cmp(const void *a, const void *b) {
+    const ent_t *x = (const ent_t *)a, *y = (const ent_t *)b;
+    return x->v < y->v ? -1 : x->v > y->v ? 1 : 0;
 }
 
-static og_graph *graph_alloc(int64_t n, int64_t nnz) {
+static og_graph *graph_alloc(int64_t n) {
     og_graph *g = (og_graph *)calloc(1, sizeof(og_graph));
     if (!g) return NULL;
     g->n = n;
-    g->nnz = nnz;
     g->row_ptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
-    g->col = (int32_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int32_t));
-    g->w = (int64_t *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int64_t));
     g->loop = (int64_t *)calloc((size_t)n, sizeof(int64_t));
     g->delta = (int64_t *)calloc((size_t)n, sizeof(int64_t));
-    if (!g->row_ptr || !g->col || !g->w || !g->loop || !g->delta) { og_graph_free(g); return NULL; }
+    if (!g->row_ptr || !g->loop || !g->delta) { og_graph_free(g); return NULL; }
     return g;
 }
 
@@ -80,23 +94,76 @@ void og_graph_free(og_graph *g) {
     free(g);
 }
 
-/* Build CSR from sorted, merged directed records (u,v,w); loops already in g->loop. */
-static void fill_csr(og_graph *g, rec_t *r, int64_t cnt) {
-    int64_t out = 0;
-    for (int64_t k = 0; k < cnt; ++k) {           /* merge duplicates by summing (D25) */
-        if (out > 0 && r[out - 1].u == r[k].u && r[out - 1].v == r[k].v) r[out - 1].w += r[k].w;
-        else r[out++] = r[k];
+/* The CSR of directed records that were bucketed by source: row u holds its records
+ * (col[k], w[k]) for k in [row_ptr[u], row_ptr[u+1]) in arbitrary order.  Sort each row
+ * by target and merge duplicates by summing (P:L271 sort_by_key + reduce_by_key; D25),
+ * compact, then δ_i = Σ_{j∈Γ(i)} ω(i,j) with a loop counted twice (D2). */
+static int finish_csr(og_graph *g) {
+    const int64_t n = g->n;
+    int64_t maxlen = 0;
+    for (int64_t u = 0; u < n; ++u)
+        if (g->row_ptr[u + 1] - g->row_ptr[u] > maxlen) maxlen = g->row_ptr[u + 1] - g->row_ptr[u];
+    int64_t *len = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    if (!len) return OG_ENOMEM;
+    int err = 0;
+#pragma omp parallel
+    {
+        ent_t *buf = (ent_t *)malloc((size_t)(maxlen > 0 ? maxlen : 1) * sizeof(ent_t));
+        if (!buf) {
+#pragma omp atomic write
+            err = 1;
+        }
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t u = 0; u < n; ++u) {
+            if (!buf) { len[u] = 0; continue; }
+            const int64_t b = g->row_ptr[u], e = g->row_ptr[u + 1];
+            for (int64_t k = b; k < e; ++k) { buf[k - b].v = g->col[k]; buf[k - b].w = g->w[k]; }
+            qsort(buf, (size_t)(e - b), sizeof(ent_t), ent_cmp);
+            int64_t out = 0;
+            for (int64_t k = 0; k < e - b; ++k) {
+                if (out > 0 && buf[out - 1].v == buf[k].v) buf[out - 1].w += buf[k].w;
+                else buf[out++] = buf[k];
+            }
+            for (int64_t k = 0; k < out; ++k) { g->col[b + k] = buf[k].v; g->w[b + k] = buf[k].w; }
+            len[u] = out;
+        }
+        free(buf);
     }
-    g->nnz = out;
-    for (int64_t k = 0; k < out; ++k) g->row_ptr[r[k].u + 1]++;
-    for (int64_t i = 0; i < g->n; ++i) g->row_ptr[i + 1] += g->row_ptr[i];   /* exclusive scan */
-    for (int64_t k = 0; k < out; ++k) { g->col[k] = r[k].v; g->w[k] = r[k].w; }
-    /* δ_i = Σ_{j∈Γ(i)} ω(i,j) with a loop counted twice (D2) */
-    for (int64_t i = 0; i < g->n; ++i) {
+    if (err) { free(len); return OG_ENOMEM; }
+    /* compact (new offsets never exceed the old ones, so an in-place forward move) */
+    int64_t o = 0;
+    for (int64_t u = 0; u < n; ++u) {
+        const int64_t b = g->row_ptr[u];
+        g->row_ptr[u] = o;
+        if (o != b) {
+            memmove(g->col + o, g->col + b, (size_t)len[u] * sizeof(int32_t));
+            memmove(g->w + o, g->w + b, (size_t)len[u] * sizeof(int64_t));
+        }
+        o += len[u];
+    }
+    g->row_ptr[n] = o;
+    g->nnz = o;
+    free(len);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
         int64_t s = 2 * g->loop[i];
         for (int64_t e = g->row_ptr[i]; e < g->row_ptr[i + 1]; ++e) s += g->w[e];
         g->delta[i] = s;
     }
+    return OG_OK;
+}
+
+/* Bucket directed records by source: row_ptr = exclusive scan of the per-row counts
+ * (already in row_ptr[u+1]); allocates col/w with `cnt` entries; returns a cursor array
+ * (next free slot of each row) or NULL. */
+static int64_t *bucket_alloc(og_graph *g, int64_t cnt) {
+    for (int64_t u = 0; u < g->n; ++u) g->row_ptr[u + 1] += g->row_ptr[u];
+    g->col = (int32_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int32_t));
+    g->w = (int64_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int64_t));
+    int64_t *cur = (int64_t *)malloc((size_t)(g->n > 0 ? g->n : 1) * sizeof(int64_t));
+    if (!g->col || !g->w || !cur) { free(cur); return NULL; }
+    memcpy(cur, g->row_ptr, (size_t)g->n * sizeof(int64_t));
+    return cur;
 }
 
 /* §5.1.2 "Neighbor computation": mirror every non-loop record, sort by
@@ -105,26 +172,30 @@ int og_graph_build(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                    const int64_t *w, og_graph **out) {
     *out = NULL;
     if (n <= 0 || m < 0) return OG_EINVAL;
-    rec_t *r = (rec_t *)malloc((size_t)(2 * m > 0 ? 2 * m : 1) * sizeof(rec_t));
-    og_graph *g = graph_alloc(n, 0);
-    if (!r || !g) { free(r); og_graph_free(g); return OG_ENOMEM; }
+    og_graph *g = graph_alloc(n);
+    if (!g) return OG_ENOMEM;
     int64_t cnt = 0, W = 0;
     for (int64_t k = 0; k < m; ++k) {
         int32_t u = src[k], v = dst[k];
         int64_t wk = w ? w[k] : 1;                 /* D1: unweighted ⇒ 1 */
-        if (u < 0 || v < 0 || u >= n || v >= n || wk <= 0) { free(r); og_graph_free(g); return OG_EGRAPH; }
+        if (u < 0 || v < 0 || u >= n || v >= n || wk <= 0) { og_graph_free(g); return OG_EGRAPH; }
         W += wk;                                    /* D3: W = Σ weights, loops once */
         if (u == v) { g->loop[u] += wk; continue; }
-        r[cnt].u = u; r[cnt].v = v; r[cnt].w = wk; ++cnt;
-        r[cnt].u = v; r[cnt].v = u; r[cnt].w = wk; ++cnt;
+        g->row_ptr[u + 1]++; g->row_ptr[v + 1]++;   /* both orientations */
+        cnt += 2;
     }
-    qsort(r, (size_t)cnt, sizeof(rec_t), rec_cmp);
-    free(g->col); free(g->w);
-    g->col = (int32_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int32_t));
-    g->w = (int64_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int64_t));
-    if (!g->col || !g->w) { free(r); og_graph_free(g); return OG_ENOMEM; }
-    fill_csr(g, r, cnt);
-    free(r);
+    int64_t *cur = bucket_alloc(g, cnt);
+    if (!cur) { og_graph_free(g); return OG_ENOMEM; }
+    for (int64_t k = 0; k < m; ++k) {
+        int32_t u = src[k], v = dst[k];
+        int64_t wk = w ? w[k] : 1;
+        if (u == v) continue;
+        g->col[cur[u]] = v; g->w[cur[u]++] = wk;
+        g->col[cur[v]] = u; g->w[cur[v]++] = wk;
+    }
+    free(cur);
+    int rc = finish_csr(g);
+    if (rc) { og_graph_free(g); return rc; }
     g->W = W;
     *out = g;
     return W > 0 ? OG_OK : OG_EZEROW;
@@ -179,14 +250,27 @@ int og_graph_build_real(int64_t n, int64_t m, const int32_t *src, const int32_t 
 
 /* ----------------------------------------------------------- community state */
 
+/* Eq. 1 scratch of one thread: e_{i→c} per label, and the list of touched labels */
+typedef struct {
+    int64_t *e;          /* e_{i→c} accumulator (Eq. 1)                */
+    uint8_t *mark;       /* c touched                                  */
+    int32_t *touched;    /* list of touched labels                     */
+} scratch_t;
+
+static int scratch_init(scratch_t *s, int64_t n) {
+    s->e = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    s->mark = (uint8_t *)calloc((size_t)n, 1);
+    s->touched = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    return s->e && s->mark && s->touched;
+}
+static void scratch_free(scratch_t *s) { free(s->e); free(s->mark); free(s->touched); }
+
 struct og_state {
     const og_graph *g;
     const int32_t *C;    /* snapshot labels (borrowed)                 */
     int64_t *deg;        /* deg_C (Eq. 2), indexed by label            */
     int64_t *size;       /* |C|, indexed by label                      */
-    int64_t *e;          /* scratch: e_{i→c} accumulator (Eq. 1)       */
-    uint8_t *mark;       /* scratch: c touched                         */
-    int32_t *touched;    /* scratch: list of touched labels            */
+    scratch_t s;         /* scratch of og_decide (single-vertex calls)  */
 };
 
 og_state *og_state_new(const og_graph *g, const int32_t *labels) {
@@ -197,10 +281,7 @@ og_state *og_state_new(const og_graph *g, const int32_t *labels) {
     st->C = labels;
     st->deg = (int64_t *)calloc((size_t)n, sizeof(int64_t));
     st->size = (int64_t *)calloc((size_t)n, sizeof(int64_t));
-    st->e = (int64_t *)calloc((size_t)n, sizeof(int64_t));
-    st->mark = (uint8_t *)calloc((size_t)n, 1);
-    st->touched = (int32_t *)malloc((size_t)n * sizeof(int32_t));
-    if (!st->deg || !st->size || !st->e || !st->mark || !st->touched) { og_state_free(st); return NULL; }
+    if (!st->deg || !st->size) { og_state_free(st); return NULL; }
     for (int64_t i = 0; i < n; ++i) {            /* Eq. 2: deg_C = Σ_{i∈C} δ_i */
         st->deg[labels[i]] += g->delta[i];
         st->size[labels[i]] += 1;
@@ -210,7 +291,7 @@ og_state *og_state_new(const og_graph *g, const int32_t *labels) {
 
 void og_state_free(og_state *st) {
     if (!st) return;
-    free(st->deg); free(st->size); free(st->e); free(st->mark); free(st->touched);
+    free(st->deg); free(st->size); scratch_free(&st->s);
     free(st);
 }
 
@@ -226,7 +307,7 @@ void og_state_free(og_state *st) {
  *   singlet rule: singlet → singlet only if l(target) < l(C(i)) (§3.1.1; D8: else stay)
  *  mode 1 (isolated merge; D14): a singlet whose neighbours lie in exactly one
  *   community T moves to T (singlet rule applies). */
-int32_t og_decide(const og_state *st, int64_t i, int32_t mode) {
+static int32_t decide(const og_state *st, scratch_t *sc, int64_t i, int32_t mode) {
     const og_graph *g = st->g;
     const int32_t *C = st->C;
     int32_t own = C[i];
@@ -236,21 +317,21 @@ int32_t og_decide(const og_state *st, int64_t i, int32_t mode) {
     int64_t nt = 0;
     for (int64_t k = b; k < eend; ++k) {             /* Eq. 1 */
         int32_t c = C[g->col[k]];
-        if (!st->mark[c]) { st->mark[c] = 1; st->touched[nt++] = c; }
-        st->e[c] += g->w[k];
+        if (!sc->mark[c]) { sc->mark[c] = 1; sc->touched[nt++] = c; }
+        sc->e[c] += g->w[k];
     }
     int32_t result = own;
     if (mode == 0) {
         i128 twoW = (i128)2 * g->W;
         i128 di = g->delta[i];
-        int64_t e_own = st->mark[own] ? st->e[own] : 0;
+        int64_t e_own = sc->mark[own] ? sc->e[own] : 0;
         i128 S_own = twoW * e_own - di * ((i128)st->deg[own] - di);
         int32_t best = -1;
         i128 S_best = 0;
         for (int64_t t = 0; t < nt; ++t) {
-            int32_t c = st->touched[t];
+            int32_t c = sc->touched[t];
             if (c == own) continue;
-            i128 S = twoW * st->e[c] - di * (i128)st->deg[c];
+            i128 S = twoW * sc->e[c] - di * (i128)st->deg[c];
             if (best < 0 || S > S_best || (S == S_best && c < best)) { best = c; S_best = S; }
         }
         if (best >= 0 && S_best > S_own) {
@@ -261,26 +342,46 @@ int32_t og_decide(const og_state *st, int64_t i, int32_t mode) {
         int32_t T = -1;
         int64_t distinct = 0;
         for (int64_t t = 0; t < nt; ++t)
-            if (st->touched[t] != own) { ++distinct; T = st->touched[t]; }
+            if (sc->touched[t] != own) { ++distinct; T = sc->touched[t]; }
         if (distinct == 1) {
             if (st->size[T] == 1 && T > own) result = own;
             else result = T;
         }
     }
-    for (int64_t t = 0; t < nt; ++t) { st->e[st->touched[t]] = 0; st->mark[st->touched[t]] = 0; }
+    for (int64_t t = 0; t < nt; ++t) { sc->e[sc->touched[t]] = 0; sc->mark[sc->touched[t]] = 0; }
     return result;
+}
+
+int32_t og_decide(og_state *st, int64_t i, int32_t mode) {
+    if (!st->s.e && !scratch_init(&st->s, st->g->n)) return -1;
+    return decide(st, &st->s, i, mode);
 }
 
 int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_out, int32_t mode) {
     og_state *st = og_state_new(g, labels_in);
     if (!st) return -1;
     int64_t moved = 0;
-    for (int64_t i = 0; i < g->n; ++i) {   /* Jacobi: every decision reads the snapshot (D9) */
-        labels_out[i] = og_decide(st, i, mode);
-        moved += labels_out[i] != labels_in[i];
+    int err = 0;
+    /* Jacobi: every decision reads only the snapshot (D9), so the vertices are
+     * independent and the loop may run on any number of threads. */
+#pragma omp parallel reduction(+ : moved)
+    {
+        scratch_t sc;
+        int ok = scratch_init(&sc, g->n);
+        if (!ok) {
+#pragma omp atomic write
+            err = 1;
+        }
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t i = 0; i < g->n; ++i) {
+            if (!ok) continue;
+            labels_out[i] = decide(st, &sc, i, mode);
+            moved += labels_out[i] != labels_in[i];
+        }
+        scratch_free(&sc);
     }
     og_state_free(st);
-    return moved;
+    return err ? -1 : moved;
 }
 
 /* ------------------------------------------------- colouring heuristic (F2, D29) */
@@ -333,9 +434,22 @@ int64_t og_sweep_colored(const og_graph *g, const int32_t *color, int32_t ncolor
     for (int32_t c = 0; c < ncolors; ++c) {
         og_state *st = og_state_new(g, cur);              /* state after class c-1 */
         if (!st) { free(cur); return -1; }
-        for (int64_t i = 0; i < n; ++i)
-            if (color[i] == c) labels_out[i] = og_decide(st, i, 0);
+        int err = 0;
+#pragma omp parallel
+        {
+            scratch_t sc;
+            int ok = scratch_init(&sc, n);
+            if (!ok) {
+#pragma omp atomic write
+                err = 1;
+            }
+#pragma omp for schedule(dynamic, 256)
+            for (int64_t i = 0; i < n; ++i)      /* Jacobi within the class */
+                if (ok && color[i] == c) labels_out[i] = decide(st, &sc, i, 0);
+            scratch_free(&sc);
+        }
         og_state_free(st);
+        if (err) { free(cur); return -1; }
         memcpy(cur, labels_out, (size_t)n * sizeof(int32_t));   /* commit class c */
     }
     for (int64_t i = 0; i < n; ++i) moved += labels_out[i] != labels_in[i];
@@ -350,13 +464,21 @@ int64_t og_sweep_colored(const og_graph *g, const int32_t *color, int32_t ncolor
 static void modularity_num(const og_graph *g, const int32_t *C, const int64_t *deg,
                            int64_t *I2, i128 *S2) {
     int64_t s = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : s)
     for (int64_t i = 0; i < g->n; ++i) {
         s += 2 * g->loop[i];
         for (int64_t k = g->row_ptr[i]; k < g->row_ptr[i + 1]; ++k)
             if (C[g->col[k]] == C[i]) s += g->w[k];
     }
-    i128 q = 0;
-    for (int64_t c = 0; c < g->n; ++c) q += (i128)deg[c] * deg[c];
+    i128 q = 0;   /* exact: int128 addition is associative (partials per thread) */
+#pragma omp parallel
+    {
+        i128 qt = 0;
+#pragma omp for schedule(static)
+        for (int64_t c = 0; c < g->n; ++c) qt += (i128)deg[c] * deg[c];
+#pragma omp critical
+        q += qt;
+    }
     *I2 = s;
     *S2 = q;
 }
@@ -406,29 +528,31 @@ int64_t og_renumber(int64_t n, const int32_t *in, int32_t *outl) {
  * inter-community weights are summed per community pair. */
 int og_induce(const og_graph *g, const int32_t *C, int64_t k, og_graph **out) {
     *out = NULL;
-    og_graph *h = graph_alloc(k, 0);
-    rec_t *r = (rec_t *)malloc((size_t)(g->nnz > 0 ? g->nnz : 1) * sizeof(rec_t));
-    int64_t *intra2 = (int64_t *)calloc((size_t)k, sizeof(int64_t));
-    if (!h || !r || !intra2) { og_graph_free(h); free(r); free(intra2); return OG_ENOMEM; }
+    og_graph *h = graph_alloc(k);
+    int64_t *intra2 = (int64_t *)calloc((size_t)(k > 0 ? k : 1), sizeof(int64_t));
+    if (!h || !intra2) { og_graph_free(h); free(intra2); return OG_ENOMEM; }
     int64_t cnt = 0;
+    for (int64_t u = 0; u < g->n; ++u) {               /* count inter entries per C(u) */
+        int32_t cu = C[u];
+        for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e)
+            if (C[g->col[e]] != cu) { h->row_ptr[cu + 1]++; ++cnt; }
+    }
+    int64_t *cur = bucket_alloc(h, cnt);
+    if (!cur) { og_graph_free(h); free(intra2); return OG_ENOMEM; }
     for (int64_t u = 0; u < g->n; ++u) {
         int32_t cu = C[u];
         h->loop[cu] += g->loop[u];
         for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e) {
             int32_t cv = C[g->col[e]];
             if (cv == cu) intra2[cu] += g->w[e];     /* each undirected edge seen twice */
-            else { r[cnt].u = cu; r[cnt].v = cv; r[cnt].w = g->w[e]; ++cnt; }
+            else { h->col[cur[cu]] = cv; h->w[cur[cu]++] = g->w[e]; }
         }
     }
+    free(cur);
     for (int64_t c = 0; c < k; ++c) h->loop[c] += intra2[c] / 2;
     free(intra2);
-    qsort(r, (size_t)cnt, sizeof(rec_t), rec_cmp);
-    free(h->col); free(h->w);
-    h->col = (int32_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int32_t));
-    h->w = (int64_t *)malloc((size_t)(cnt > 0 ? cnt : 1) * sizeof(int64_t));
-    if (!h->col || !h->w) { free(r); og_graph_free(h); return OG_ENOMEM; }
-    fill_csr(h, r, cnt);
-    free(r);
+    int rc = finish_csr(h);                          /* sort by (C(u), C(v)), sum */
+    if (rc) { og_graph_free(h); return rc; }
     h->W = g->W;
     *out = h;
     /* W' = W (weight conservation): Σ directed inter weights / 2 + Σ loops */

@@ -91,7 +91,7 @@ og_state *og_state_new(const og_graph *g, const int32_t *labels);
 void      og_state_free(og_state *st);
 /* Decision of one vertex against the snapshot `st` (Eq. 5 + heuristics).
  * mode 0 = local-move decision, mode 1 = isolated-merge decision. */
-int32_t   og_decide(const og_state *st, int64_t i, int32_t mode);
+int32_t   og_decide(og_state *st, int64_t i, int32_t mode);   /* -1: out of memory */
 
 /* One Jacobi sweep (mode 0) or one merge batch (mode 1) over all vertices from the
  * snapshot labels_in; writes labels_out; returns the number of vertices that moved. */
@@ -137,6 +137,11 @@ void    og_result_trace(const og_result *r, int32_t l, int64_t *moved, double *q
 int64_t og_result_edge_visits(const og_result *r);
 
 void og_config_default(og_config *cfg);
+
+/* OpenMP threads of the schedule-independent loops (see oracle.c's header); 1 = the
+ * single-threaded oracle.  Results do not depend on it. */
+void    og_set_threads(int32_t t);
+int32_t og_get_threads(void);
 
 #ifdef __cplusplus
 }

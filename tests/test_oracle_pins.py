@@ -394,3 +394,90 @@ def test_theta_schedule_cycles():
     assert a.sweeps == b.sweeps and np.array_equal(a.final, b.final)
     c = oracle.run(g, theta_schedule=[1e-6, 1e-1])
     assert c.sweeps[0] == oracle.run(g).sweeps[0]
+
+
+@pytest.mark.parametrize("merge", [True, False])
+def test_karate_exact_alg1_abs(merge):
+    """Exact karate values of SURVEY Appendix A (an independent exact-rational simulation of
+    §8(c)): Q = 1253/3042, sweeps [100, 2], the level label arrays and the final partition;
+    the 99-sweep cap gives 4939/12168 (the Jacobi 2-cycle, reading D12)."""
+    from fractions import Fraction
+    gold = json.load(open(os.path.join(GOLD, "karate.json")))
+    ex = gold["alg1_abs"]
+    r = inputs.karate()
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst)
+    res = oracle.run(g, merge_isolated=merge)
+    assert res.final_q == float(Fraction(*ex["final_q_fraction"]))
+    assert res.sweeps == ex["sweeps"]
+    assert [lv.tolist() for lv in res.levels] == ex["levels"]
+    assert res.final.tolist() == ex["final"]
+    assert np.allclose(res.q, ex["q_levels"], rtol=0, atol=5e-11)
+    res99 = oracle.run(g, max_sweeps=99, merge_isolated=merge)
+    assert res99.final_q == float(Fraction(*gold["cap99_final_q_fraction"]))
+
+
+def test_karate_exact_signed():
+    from fractions import Fraction
+    gold = json.load(open(os.path.join(GOLD, "karate.json")))
+    ex = gold["signed"]
+    r = inputs.karate()
+    res = oracle.run(oracle.Graph.from_edges(r.n, r.src, r.dst), stop_rule=1)
+    assert res.final_q == float(Fraction(*ex["final_q_fraction"]))
+    assert res.sweeps == ex["sweeps"]
+    assert res.final.tolist() == ex["final"]
+    assert np.allclose(res.q, ex["q_levels"], rtol=0, atol=5e-11)
+
+
+def _run_all(rec, threads, **kw):
+    oracle.set_threads(threads)
+    try:
+        g = oracle.Graph.from_edges(rec.n, rec.src, rec.dst, rec.w)
+        res = oracle.run(g, **kw)
+        return g.arrays(), res
+    finally:
+        oracle.set_threads(os.cpu_count() or 1)
+
+
+@pytest.mark.parametrize("rec", [lambda: inputs.rmat(14, 16, seed=7),
+                                 lambda: inputs.cooc(topics=60, topic_size=200, docs=60_000, seed=3),
+                                 lambda: inputs.sbm(20_000, 20, 32, 0.3, seed=2)],
+                         ids=["rmat14", "cooc", "sbm20k"])
+def test_oracle_threads_bit_identical(rec):
+    """The OpenMP loops (Jacobi sweep, exact Eq. 3 sums, per-row sorts) cannot change any
+    result: 1 thread and several threads give the same CSR, levels, Q bits and traces."""
+    r = rec()
+    a1, r1 = _run_all(r, 1)
+    a4, r4 = _run_all(r, 4)
+    for k in ("row_ptr", "col", "w", "loop", "delta"):
+        assert np.array_equal(a1[k], a4[k]), k
+    assert a1["W"] == a4["W"]
+    assert r1.sweeps == r4.sweeps and r1.q == r4.q and r1.edge_visits == r4.edge_visits
+    for x, y in zip(r1.levels, r4.levels):
+        assert np.array_equal(x, y)
+    for (m1, q1), (m4, q4) in zip(r1.traces, r4.traces):
+        assert np.array_equal(m1, m4) and np.array_equal(q1, q4)
+    # and the colouring heuristic's class sweeps (D29)
+    c1 = _run_all(r, 1, coloring=True, color_cap_min_n=0, color_classes=8)[1]
+    c4 = _run_all(r, 4, coloring=True, color_cap_min_n=0, color_classes=8)[1]
+    assert c1.sweeps == c4.sweeps and c1.q == c4.q
+    assert np.array_equal(c1.final, c4.final)
+
+
+def test_oracle_build_matches_global_sort():
+    """The counting-sort-by-source + per-row sort of og_graph_build equals the textbook
+    construction (numpy lexsort of both orientations, duplicates summed)."""
+    r = inputs.rmat(12, 16, seed=11)
+    g = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w).arrays()
+    s, d, w = r.src.astype(np.int64), r.dst.astype(np.int64), r.w.astype(np.int64)
+    nl = s != d
+    u = np.concatenate([s[nl], d[nl]]); v = np.concatenate([d[nl], s[nl]]); ww = np.concatenate([w[nl], w[nl]])
+    key = u * r.n + v
+    uk, inv = np.unique(key, return_inverse=True)
+    ws = np.zeros(len(uk), np.int64)
+    np.add.at(ws, inv, ww)
+    assert np.array_equal(g["col"], (uk % r.n).astype(np.int32))
+    assert np.array_equal(g["w"], ws)
+    assert np.array_equal(g["row_ptr"], np.searchsorted(uk // r.n, np.arange(r.n + 1)))
+    loops = np.zeros(r.n, np.int64)
+    np.add.at(loops, s[~nl], w[~nl])
+    assert np.array_equal(g["loop"], loops)

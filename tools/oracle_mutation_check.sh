@@ -24,7 +24,9 @@ mut 's/h->loop\[c\] += intra2\[c\] \/ 2;/h->loop[c] += intra2[c];/' "induce doub
 mut 's/id\[c\] = used\[c\] ? (int32_t)k++ : -1;/id[c] = used[c] ? (int32_t)(k++) : -1; if (used[c] \&\& k > 1) id[c] = (int32_t)(k - 1) ^ 1;/' "renumber not order-preserving (D18)"
 mut 's/if (mode == 1 \&\& st->size\[own\] != 1) return own;/if (0) return own;/' "merge non-singlets (D14)"
 mut 's/st->deg\[labels\[i\]\] += g->delta\[i\];/st->deg[labels[i]] += 1;/' "deg as count (Eq.2)"
-mut 's/i128 S = twoW \* st->e\[c\] - di \* (i128)st->deg\[c\];/i128 S = twoW * st->e[c] + di * (i128)st->deg[c];/' "sign flip in S (Eq.4)"
+mut 's/i128 S = twoW \* sc->e\[c\] - di \* (i128)st->deg\[c\];/i128 S = twoW * sc->e[c] + di * (i128)st->deg[c];/' "sign flip in S (Eq.4)"
+mut 's/if (out > 0 \&\& buf\[out - 1\].v == buf\[k\].v) buf\[out - 1\].w += buf\[k\].w;/if (out > 0 \&\& buf[out - 1].v == buf[k].v) buf[out - 1].w = buf[k].w;/' "duplicates not summed (D25)"
+mut 's/for (int64_t t = 0; t < nt; ++t) { sc->e\[sc->touched\[t\]\] = 0; sc->mark\[sc->touched\[t\]\] = 0; }/for (int64_t t = 0; t < nt; ++t) { sc->mark[sc->touched[t]] = 0; }/' "Eq.1 scratch not reset between vertices"
 mut 's/for (s = 1; s <= cfg->max_sweeps; ++s) {/for (s = 1; s <= cfg->max_sweeps - 1; ++s) {/' "cap off by one (D12)"
 mut 's/if (l == 0 || !(Ql - mod_curr < cfg->big_theta))/if (!(Ql - mod_curr < cfg->big_theta))/' "level 0 not forced (Alg.2)"
 mut 's/return neg ? -d : d;/return d;/' "d128 sign lost (D22)"
