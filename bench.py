@@ -32,15 +32,15 @@ METRIC = "local-move edges/sec and end-to-end Louvain time at 1/2/4/8 B200; fina
 UNIT = "edges/s"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
-# bounded CPU-baseline sample: the oracle's full run (CSR build + all levels) on a
-# smaller graph of the same recipe (10-30 s single-threaded on the GPU box host)
-CPU_SAMPLE = {
-    "rmat24": ("rmat", dict(scale=18, edge_factor=16, seed=4), "R-MAT scale 18, ef 16, weights 1-16 (C4 recipe)"),
-    "rmat27": ("rmat", dict(scale=18, edge_factor=16, seed=5), "R-MAT scale 18, ef 16, weights 1-16 (C5 recipe)"),
-    "sbm": ("sbm", dict(n=100_000, blocks=100, avg_deg=32, mu=0.3, seed=2), "SBM n=100k, blocks of 1000, deg 32, mu 0.3"),
-    "cooc": ("cooc", dict(topics=250, topic_size=1000, docs=875_000, seed=3), "co-occurrence at 1/20 scale (C3 recipe)"),
-    "karate": ("karate", {}, "karate (full workload)"),
-}
+# CPU baseline (SURVEY §8(d) "oracle timing: same run, same CSR bytes"): the oracle as it
+# stands builds its own CSR of the SAME workload (same seeded records) and runs the first
+# sweeps of Algorithm 1 at level 0 — a bounded sample of the same step (the whole run
+# would take minutes), timed on 1 core and on every host core (bit-identical results).
+# rmat27 (C5) needs ~120 GB of host memory for the oracle's CSR: it keeps a same-recipe
+# R-MAT scale-24 sample instead (same_config false).
+CPU_SWEEPS_1CORE = 1
+CPU_SWEEPS_ALL = 3
+REF_SWEEPS = 2  # --impl reference: sweeps per step (Algorithm 1 at level 0, all cores)
 
 
 def peaks():
@@ -128,44 +128,112 @@ def barrier(world):
     lvd.barrier()
 
 
-def cpu_baseline(workload, budget_note=True):
-    """Time the oracle as it stands (single thread) on a bounded sample of the workload."""
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+_ORACLE_G = {}
+
+
+def oracle_graph(workload, records=None):
+    """The oracle's own CSR of the workload (built from the seeded records, never from
+    the CUDA path), cached per process; returns (graph, build seconds, description)."""
     import oracle
     from paper_1805_10904_b200 import inputs
 
-    kind, kw, desc = CPU_SAMPLE[workload]
-    r = getattr(inputs, kind)(**kw)
+    if workload not in _ORACLE_G:
+        same = workload != "rmat27"
+        r = records if (same and records is not None) else (inputs.make(workload) if same else inputs.rmat(24, 16, seed=5))
+        oracle.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        g = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+        dt = time.perf_counter() - t0
+        desc = workload if same else "R-MAT scale 24 of the C5 recipe (seed 5)"
+        _ORACLE_G[workload] = (g, dt, desc, same)
+    return _ORACLE_G[workload]
+
+
+def oracle_sweeps(g, threads, sweeps):
+    """Algorithm 1 at level 0, capped at `sweeps` sweeps (+ merge, renumber, Q)."""
+    import oracle
+
+    oracle.set_threads(threads)
     t0 = time.perf_counter()
-    g = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
-    res = oracle.run(g)
+    res = oracle.run(g, max_sweeps=sweeps, max_levels=1)
     dt = time.perf_counter() - t0
-    return {"value": res.edge_visits / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle full run (CSR build + all levels) on {desc}: {res.edge_visits} edge visits "
-                      f"in {dt:.2f} s, Q={res.final_q:.6f}", "seconds": dt}
+    oracle.set_threads(os.cpu_count() or 1)
+    return res.edge_visits, dt
+
+
+def cpu_baseline(workload, records=None):
+    """The oracle as it stands, on the same workload's CSR, 1 core and all host cores."""
+    g, tb, desc, same = oracle_graph(workload, records)
+    ncore = os.cpu_count() or 1
+    v1, t1 = oracle_sweeps(g, 1, CPU_SWEEPS_1CORE)
+    va, ta = oracle_sweeps(g, ncore, CPU_SWEEPS_ALL)
+    return {"value": va / ta, "unit": UNIT, "cores": ncore, "kind": "oracle",
+            "sample": f"oracle (OpenMP over the Jacobi sweep, {ncore} threads) on {desc} "
+                      f"(n={g.n}, nnz={g.nnz}, the oracle's own CSR of the same records): level-0 Algorithm 1 "
+                      f"capped at {CPU_SWEEPS_ALL} sweeps (+merge, renumber, Q) = {va} edge visits in {ta:.2f} s",
+            "same_config": same,
+            "single_core": {"value": v1 / t1, "unit": UNIT, "cores": 1,
+                            "sample": f"same, 1 thread, {CPU_SWEEPS_1CORE} sweep(s): {v1} edge visits in {t1:.2f} s"},
+            "oracle_csr_build_s": round(tb, 2), "cpu_model": cpu_model(), "nproc": ncore}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, each step a bounded sample."""
-    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """--impl reference: the CPU oracle as it stands (all host cores) on the same workload;
+    each step = Algorithm 1 at level 0 capped at REF_SWEEPS sweeps on the oracle's CSR
+    (built once, untimed, from the same seeded records)."""
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass  # the oracle has no warm-up state; one untimed step is not needed
-    times, visits, last = [], 0, None
+    g, tb, desc, same = oracle_graph(args.workload)
+    ncore = os.cpu_count() or 1
+    for _ in range(min(args.warmup, 1)):
+        oracle_sweeps(g, ncore, 1)
+    times, visits = [], 0
     for _ in range(args.steps):
-        b = cpu_baseline(args.workload)
-        times.append(b["seconds"])
-        visits = b["value"] * b["seconds"]
-        last = b
+        v, dt = oracle_sweeps(g, ncore, REF_SWEEPS)
+        times.append(dt)
+        visits = v
     T = sum(times) / len(times)
+    sample = (f"oracle (OpenMP, {ncore} threads) on {desc} (n={g.n}, nnz={g.nnz}): per step level-0 Algorithm 1 "
+              f"capped at {REF_SWEEPS} sweeps (+merge, renumber, Q) = {visits} edge visits; CSR built once "
+              f"({tb:.1f} s, untimed)")
     line = {"impl": "reference", "metric": METRIC, "value": visits / T, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": T * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "sample": last["sample"]},
-            "cpu_baseline": {"value": visits / T, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": last["sample"]},
+            "config": {"workload": args.workload, "sample": sample, "same_config": same},
+            "cpu_baseline": {"value": visits / T, "unit": UNIT, "cores": ncore, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": visits / T, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_local_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N local ranks (one per GPU) with the
+    torchrun environment (127.0.0.1 rendezvous), forward rank 0's output, return the
+    worst exit code.  Under torchrun (WORLD_SIZE set) this is not used."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(p.wait() for p in procs)
 
 
 def main():
@@ -177,9 +245,24 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--dist-check", action="store_true",
+                    help="launcher self-test (CPU, gloo): every rank joins, rank 0 prints world and max over ranks")
     ap.add_argument("--coloring-steps", type=int, default=1,
                     help="timed steps of the colouring-heuristic variant (SURVEY F2, D29); 0 = skip")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_local_ranks(args.gpus)
+    if args.dist_check:
+        from paper_1805_10904_b200 import dist as lvd
+
+        rank, world, _ = lvd.env_rank()
+        if world > 1:
+            lvd.init_process_group("gloo")
+        mx = lvd.allmax(float(rank), device="cpu")
+        lvd.barrier()
+        if rank == 0:
+            print(json.dumps({"dist_check": True, "n_gpus": world, "allmax_rank": mx, "gpus_arg": args.gpus}), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
 
@@ -189,6 +272,11 @@ def main():
     from paper_1805_10904_b200 import Louvain
 
     world, rank, local = dist_init()
+    if world > torch.cuda.device_count():
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "error": f"{world} ranks but {torch.cuda.device_count()} visible GPUs "
+                              "(one process per GPU)"}), flush=True)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     r = make_workload(args.workload)
@@ -348,9 +436,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline(args.workload)
-            cpu.pop("seconds", None)
-            cpu["cores_note"] = f"single-threaded oracle; host has {os.cpu_count()} cores"
+            cpu = cpu_baseline(args.workload, r)
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
     inf = infos[-1]

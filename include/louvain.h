@@ -198,7 +198,8 @@ louvain_status louvain_get_csr(louvain_t h, int64_t *nnz, int64_t *row_ptr, int3
 /* Contract level 0 by a dense partition (labels in [0,k)), like the induce step
  * (P:L306-313), and return the contracted graph's CSR through louvain_get_csr-style
  * host buffers (row_ptr k+1, col/w nnz_out).  Call once with col == NULL to get
- * *nnz_out, then again with buffers. */
+ * *nnz_out, then again with buffers.  labels: host, n entries; a label outside [0,k)
+ * returns LV_EINVAL before anything is contracted. */
 louvain_status louvain_contract(louvain_t h, const int32_t *labels, int64_t k, int64_t *nnz_out,
                                 int64_t *row_ptr, int32_t *col, int64_t *w, int64_t *loop,
                                 int64_t *delta);

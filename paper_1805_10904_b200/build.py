@@ -17,7 +17,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(CSRC, "liblouvain.so")
 SOURCES = ["lv_api.cu"]
-HEADERS = ["lv_common.cuh", "lv_scan.cuh", "lv_agg.cuh", "lv_bins.cuh", "lv_graph.cuh"]
+# every header in csrc/ is a dependency (a header edited alone must rebuild the .so)
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

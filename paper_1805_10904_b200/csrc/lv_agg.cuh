@@ -410,8 +410,11 @@ struct Acc {
 
 // Record a move own -> tgt of vertex r (weighted degree di) in the next-state deg/size
 // ("remove ... from the old community ... insert ... into the new").
-// (In the sweep-sharded mode deg_next is NULL: every rank applies all moves after the
-// label exchange instead, see k_apply_moves.)
+// The passes normally leave deg_next NULL and apply every move afterwards with
+// warp-aggregated atomics (k_apply_moves): a sweep moves millions of vertices into the
+// same few large communities, and per-move atomics on those few addresses serialise in L2
+// (measured r2: the <= 4-entry bin spent ~0.6 of its 0.8 ms on them).  The direct path
+// (deg_next set) remains for callers that want it.
 __device__ __forceinline__ void record_move(const AggArgs &a, int32_t own, int32_t tgt, i64 di) {
   if (!a.deg_next) return;
   atomicAdd((u64 *)&a.deg_next[own], (u64)(-di));
@@ -1423,20 +1426,118 @@ __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {
   if (MODE != M_EMIT) acc.flush(a.counters);
 }
 
-// Apply every move cur -> nxt to the next-state deg/size (sweep-sharded mode: run
-// identically on every rank after the label exchange; exact atomics, order-free).
-__global__ void __launch_bounds__(256) k_apply_moves(i64 n, const int32_t *__restrict__ cur,
-                                                     const int32_t *__restrict__ nxt, const i64 *__restrict__ delta,
-                                                     i64 *deg_next, int32_t *size_next) {
-  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
-    const int32_t a = cur[i], b = nxt[i];
-    if (a != b) {
-      const i64 d = delta[i];
-      atomicAdd((u64 *)&deg_next[a], (u64)(-d));
-      atomicAdd((u64 *)&deg_next[b], (u64)d);
-      atomicSub(&size_next[a], 1);
-      atomicAdd(&size_next[b], 1);
+// Apply every move cur -> nxt of a pass to the next-state deg/size (remove from
+// the old community, insert into the new), after the pass (and, sweep-sharded, after the
+// label exchange: identical on every rank).  Exact and order-free (integer sums).
+// A sweep moves millions of vertices into and out of the same few big communities, and
+// per-move global atomics on those addresses serialise in L2, so the moves are combined
+// in two stages before they reach global memory:
+//  1. the lanes of a warp that share a community (__match_any_sync) sum their δ (the
+//     16-bit halves with two 32-bit reductions: exact for δ < 2^32, "narrow");
+//  2. a CTA sweeps a chunk of AM_CHUNK vertices (AM_U per thread and step, loads issued
+//     together); the warp sums for HOT communities (snapshot deg_C >= AM_HOT, from cpk) go
+//     to a shared-memory table (fire-and-forget 32-bit reductions of the 16-bit halves:
+//     < AM_CHUNK·2^16 < 2^31 per chunk), flushed with one global atomic per hot community
+//     and chunk; cold communities (and hot ones whose probe fails, and everything when
+//     not narrow) take global atomics directly.
+constexpr int AM_T = 512, AM_TLG = 11, AM_TS = 1 << AM_TLG, AM_PROBE = 8, AM_U = 4;
+constexpr i64 AM_CHUNK = (i64)AM_T * AM_U * 4;  // 8192 vertices: 4 iterations of AM_U per thread
+constexpr size_t AM_SMEM = (size_t)AM_TS * 24;
+constexpr uint32_t AM_HOT = 1u << 12;
+
+__device__ __forceinline__ void am_global(i64 *deg_next, int32_t *size_next, int32_t c, u64 d, int cnt) {
+  atomicAdd((u64 *)&deg_next[c], d);
+  atomicAdd(&size_next[c], cnt);
+}
+
+__global__ void __launch_bounds__(AM_T) k_apply_moves(i64 n, const int32_t *__restrict__ cur,
+                                                      const int32_t *__restrict__ nxt, const i64 *__restrict__ delta,
+                                                      const uint32_t *__restrict__ cpk, i64 *deg_next,
+                                                      int32_t *size_next, int narrow) {
+  extern __shared__ __align__(16) unsigned char sm[];  // AM_SMEM bytes
+  uint32_t(*tv)[4] = (uint32_t(*)[4])sm;              // Σ lo16(+δ), Σ hi(+δ), Σ lo16(−δ), Σ hi(−δ)
+  int32_t *tk = (int32_t *)(sm + (size_t)AM_TS * 16);
+  int32_t *tc = (int32_t *)(sm + (size_t)AM_TS * 20);  // Σ ±1
+  const int lane = threadIdx.x & 31;
+  const uint32_t kb = saddr(tk);
+  for (int s = threadIdx.x; s < AM_TS; s += AM_T) {
+    tk[s] = EMPTY;
+    tv[s][0] = tv[s][1] = tv[s][2] = tv[s][3] = 0;
+    tc[s] = 0;
+  }
+  __syncthreads();
+  // one warp group's (community c, hot?, sign, Σδ halves, count) -> table or global
+  auto put = [&](int32_t c, bool hot, int neg, uint32_t lo, uint32_t hi, int cnt) {
+    if (hot) {
+      unsigned h = hslot(c, AM_TLG);
+#pragma unroll 1
+      for (int p = 0; p < AM_PROBE; ++p) {
+        int32_t k = lds_i32(kb + 4 * h);
+        if (k == EMPTY) k = cas_s32(kb + 4 * h, EMPTY, c);
+        if (k == EMPTY || k == c) {
+          red_add_s32(saddr(&tv[h][2 * neg]), lo);
+          red_add_s32(saddr(&tv[h][2 * neg + 1]), hi);
+          red_add_s32(saddr(&tc[h]), (uint32_t)(neg ? -cnt : cnt));
+          return;
+        }
+        h = (h + 1) & (AM_TS - 1);
+      }
     }
+    const u64 v = (u64)lo + ((u64)hi << 16);
+    am_global(deg_next, size_next, c, neg ? (u64)0 - v : v, neg ? -cnt : cnt);
+  };
+  for (i64 c0 = (i64)blockIdx.x * AM_CHUNK; c0 < n; c0 += (i64)gridDim.x * AM_CHUNK) {
+    const i64 c1 = c0 + AM_CHUNK < n ? c0 + AM_CHUNK : n;
+    for (i64 base = c0 + (threadIdx.x & ~31) * AM_U; base < c1; base += (i64)AM_T * AM_U) {  // warp-uniform
+      int32_t av[AM_U], bv[AM_U];
+      i64 dv[AM_U];
+      uint32_t ha[AM_U], hb[AM_U];
+#pragma unroll
+      for (int u = 0; u < AM_U; ++u) {  // every load of the AM_U vertices issued together
+        const i64 i = base + u * 32 + lane;
+        av[u] = bv[u] = 0;
+        dv[u] = 0;
+        if (i < c1) { av[u] = cur[i]; bv[u] = nxt[i]; dv[u] = delta[i]; }
+      }
+#pragma unroll
+      for (int u = 0; u < AM_U; ++u) {
+        ha[u] = hb[u] = 0;
+        if (narrow && av[u] != bv[u]) { ha[u] = __ldg(&cpk[av[u]]); hb[u] = __ldg(&cpk[bv[u]]); }
+      }
+#pragma unroll
+      for (int u = 0; u < AM_U; ++u) {
+        const bool moved = av[u] != bv[u];
+        const unsigned mv = __ballot_sync(0xffffffffu, moved);
+        if (!moved) continue;
+        const i64 d = dv[u];
+        const int32_t a = av[u], b = bv[u];
+        if (narrow) {
+          const uint32_t dlo = (uint32_t)(d & 0xFFFF), dhi = (uint32_t)((u64)d >> 16);
+          const unsigned pt = __match_any_sync(mv, b);
+          const uint32_t tlo = __reduce_add_sync(pt, dlo), thi = __reduce_add_sync(pt, dhi);
+          if (lane == __ffs(pt) - 1) put(b, (hb[u] & DEG_SAT) >= AM_HOT, 0, tlo, thi, __popc(pt));
+          const unsigned po = __match_any_sync(mv, a);
+          const uint32_t olo = __reduce_add_sync(po, dlo), ohi = __reduce_add_sync(po, dhi);
+          if (lane == __ffs(po) - 1) put(a, (ha[u] & DEG_SAT) >= AM_HOT, 1, olo, ohi, __popc(po));
+        } else {  // wide graphs (rare): per-vertex atomics
+          am_global(deg_next, size_next, b, (u64)d, 1);
+          am_global(deg_next, size_next, a, (u64)0 - (u64)d, -1);
+        }
+      }
+    }
+    __syncthreads();  // flush the chunk's hot communities, reset the table
+    for (int s = threadIdx.x; s < AM_TS; s += AM_T) {
+      const int32_t c = tk[s];
+      if (c == EMPTY) continue;
+      const u64 pv = (u64)tv[s][0] + ((u64)tv[s][1] << 16), mvv = (u64)tv[s][2] + ((u64)tv[s][3] << 16);
+      const u64 v = pv - mvv;
+      if (v) atomicAdd((u64 *)&deg_next[c], v);
+      if (tc[s]) atomicAdd(&size_next[c], tc[s]);
+      tk[s] = EMPTY;
+      tv[s][0] = tv[s][1] = tv[s][2] = tv[s][3] = 0;
+      tc[s] = 0;
+    }
+    __syncthreads();
   }
 }
 

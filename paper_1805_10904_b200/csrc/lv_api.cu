@@ -105,10 +105,13 @@ __global__ void k_init_state(i64 n, int32_t *l0, int32_t *l1, i64 *deg, int32_t 
   }
 }
 
-__global__ void k_state_from_labels(i64 n, const int32_t *lab, const i64 *delta, i64 *deg, int32_t *size, int *err) {
+// deg/size of a caller-given labelling; labels outside [0, k) set *err (and are skipped,
+// so deg/size of length k are never written out of bounds)
+__global__ void k_state_from_labels(i64 n, i64 k, const int32_t *lab, const i64 *delta, i64 *deg, int32_t *size,
+                                    int *err) {
   for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
     const int32_t c = lab[i];
-    if (c < 0 || c >= n) { atomicOr(err, 1); continue; }
+    if (c < 0 || c >= k) { atomicOr(err, 1); continue; }
     atomicAdd((u64 *)&deg[c], (u64)delta[i]);
     atomicAdd(&size[c], 1);
   }
@@ -138,6 +141,87 @@ struct DegArr {
 template <class T>
 __global__ void k_to_i64(i64 n, const T *a, i64 *b) {
   for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) b[i] = (i64)a[i];
+}
+
+// ---- device-resident Algorithm 1 loop (a CUDA graph with a conditional WHILE node).
+// The host loop of one_level() costs a D2H copy and a stream synchronisation per sweep;
+// on small levels (C1, C2) that dominates.  Here the stop test of Alg. 1 (P:L227-232,
+// readings D10-D13) runs on the device with the identical fp64 expression: the same
+// pinned int128 -> fp64 split (D22) with explicitly rounded operations (__dmul_rn,
+// __dadd_rn, __ddiv_rn, __dsub_rn: no FMA contraction), so every Q and every stop
+// decision is bit-identical to the host's (and the oracle's).
+struct DevLoop {
+  double qp;     // Q of the previous committed state
+  int32_t first; // no test yet (D11)
+  int32_t s;     // the tentative sweep the next pass computes
+  int32_t sweeps, commit, passes, cont;
+  u64 moved;     // vertices moved by the last pass
+};
+
+__device__ double d128_dev(i128 x) {
+  const bool neg = x < 0;
+  const u128 m = neg ? (u128)(-x) : (u128)x;
+  const double d = __dadd_rn(__dmul_rn(__ull2double_rn((u64)(m >> 64)), 18446744073709551616.0),
+                             __ull2double_rn((u64)m));
+  return neg ? -d : d;
+}
+
+__device__ bool stop_test_dev(int rule, double Q, double Qp, double theta) {
+  const double dq = __dsub_rn(Q, Qp);
+  if (rule == 0) {
+    if (fabs(Qp) >= 1e-12) return fabs(__ddiv_rn(dq, Qp)) < theta;
+    return fabs(dq) < theta;
+  }
+  if (fabs(Qp) >= 1e-12) return __ddiv_rn(dq, fabs(Qp)) < theta;
+  return dq < theta;
+}
+
+// After tentative sweep s: the pass's counters hold the exact Eq. 3 numerators of the
+// committed state s-1.  Same logic as one_level()'s host loop.
+__global__ void k_alg1_test(const u64 *ctr, int nbin, i64 W, u64 lsum, u64 s2i_hi, u64 s2i_lo, double theta,
+                            int rule, int max_sweeps, DevLoop *L, cudaGraphConditionalHandle hnd) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  u64 i2 = 0, moved = 0;
+  u128 s2 = 0;
+  for (int b = 0; b < nbin; ++b) {
+    i2 += ctr[8 * b];
+    moved += ctr[8 * b + 1];
+    s2 += ((u128)ctr[8 * b + 3] << 64) | ctr[8 * b + 2];
+  }
+  const i128 I2 = (i128)i2 + (i128)2 * (i128)lsum;
+  const i128 S2 = (i128)(s2 + (((u128)s2i_hi << 64) | s2i_lo));
+  const double Q = __ddiv_rn(d128_dev((i128)2 * W * I2 - S2), d128_dev((i128)4 * W * W));
+  L->passes += 1;
+  const bool stop = !L->first && stop_test_dev(rule, Q, L->qp, theta);
+  L->first = 0;
+  L->qp = Q;
+  int cont;
+  if (stop) {  // drop sweep s: the literal algorithm stopped after s-1
+    L->commit = 0;
+    cont = 0;
+  } else {
+    L->commit = 1;
+    L->sweeps = L->s;
+    cont = moved != 0 && L->s < max_sweeps;
+  }
+  L->moved = moved;
+  L->s += 1;
+  L->cont = cont;
+  cudaGraphSetConditional(hnd, cont ? 1u : 0u);
+}
+
+// Commit (D13) without a buffer flip: the next state is copied into the snapshot buffers
+// (the graph body is static, so it always reads buffer 0 and writes buffer 1).
+__global__ void k_commit_copy(i64 n, const DevLoop *L, int32_t *lab0, const int32_t *lab1, i64 *deg0,
+                              const i64 *deg1, int32_t *size0, const int32_t *size1, uint32_t *cpk0,
+                              const uint32_t *cpk1) {
+  if (!L->commit) return;
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) {
+    lab0[i] = lab1[i];
+    deg0[i] = deg1[i];
+    size0[i] = size1[i];
+    cpk0[i] = cpk1[i];
+  }
 }
 
 }  // namespace
@@ -245,8 +329,8 @@ struct SweepOut {
 // Algorithmic bytes of one launch of a sweep kernel: per directed edge
 // col 4 + weight wb + the neighbour's packed entry 8 (label, singlet bit, deg_C); per
 // active vertex 40 (row header 16, own entry 8, δ 8, deg_i 4, label_next 4).  Per pass:
-// next-state copy 24 B, packing 16 B (label 4 + cpk 4 + entry 8) and the cpk rebuild
-// 16 B (deg 8 + size 4 + cpk 4) per vertex.
+// next-state copy 24 B, packing 16 B (label 4 + cpk 4 + entry 8), the move application
+// 16 B (labels 8 + δ 8) and the cpk rebuild 16 B (deg 8 + size 4 + cpk 4) per vertex.
 double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, const std::vector<struct SweepOut> &pb,
                         u64 moved);
 
@@ -306,8 +390,10 @@ Plan plan_of(Bins &B) {  // unsharded view of existing bins (step-level entry po
 // rows' labels are carried into the next buffer first; counters hold the class's ΔI2 terms.
 // colored passes accumulate into the caller's (zeroed) counter block cctr and return
 // without a host sync (the caller reads all classes' counters once per sweep).
+// enqueue_only: leave the counters on the device (the graph-resident loop reads them there).
 SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int mode, KTimer *tm = nullptr,
-                  std::vector<SweepOut> *per_bin = nullptr, bool colored = false, u64 *cctr = nullptr) {
+                  std::vector<SweepOut> *per_bin = nullptr, bool colored = false, u64 *cctr = nullptr,
+                  bool enqueue_only = false) {
   Ctx &c = h->c;
   const int nloc = (int)P.parts.size();
   const size_t SLOT = (size_t)NBIN * 8;
@@ -325,8 +411,10 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
   a.ldeg = st.ldeg.p;
   i64 *deg_next = st.deg[st.cur ^ 1].p;
   int32_t *size_next = st.size[st.cur ^ 1].p;
-  a.deg_next = P.sharded ? nullptr : deg_next;  // sharded: all moves applied after the exchange
-  a.size_next = P.sharded ? nullptr : size_next;
+  // every move is applied after the pass (k_apply_moves, warp-aggregated; sharded: after
+  // the exchange), not by per-move atomics inside the sweep kernels
+  a.deg_next = nullptr;
+  a.size_next = nullptr;
   if (tm && mode == M_SWEEP) tm->begin(c.s, "sweep_pass");
   if (tm) tm->begin(c.s, "next_state_copy");
   if (colored) {
@@ -353,9 +441,11 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
     LV_CUDA(cudaStreamSetAttribute(c.s, cudaStreamAttributeAccessPolicyWindow, &v));
   }
   const bool narrow = g.max_delta < ((i64)1 << 32);  // e_{i->C} <= δ_i
+  // every score |S| <= 2W·δ_i (see row_s64): int64 for the whole pass when 2W·max δ < 2^63
+  const bool s64all = (u128)(u64)a.twoW * (u128)(u64)g.max_delta < ((u128)1 << 63);
   for (int j = 0; j < nloc; ++j) {
     a.counters = colored ? cctr : h->dctr.p + (size_t)j * SLOT;
-    if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, *P.parts[j], a, tm);
+    if (mode == M_SWEEP) launch_agg_wt<M_SWEEP>(c, g.wt, narrow, *P.parts[j], a, tm, s64all);
     else launch_agg_wt<M_MERGE>(c, g.wt, narrow, *P.parts[j], a, tm);
   }
   int nsum = nloc;
@@ -376,11 +466,18 @@ SweepOut run_pass(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, int
     nsum = h->world;
     src = h->dctr.p + SLOT;
   }
-  if (P.sharded)  // identical on every rank: apply all moves to the next-state deg/size
-    LV_LAUNCH(c, k_apply_moves, grid_for(c, g.n), 256, 0, g.n, label, a.label_next, g.delta.p, deg_next, size_next);
+  // apply all moves to the next-state deg/size (identical on every rank when sharded)
+  if (tm) tm->begin(c.s, "apply_moves");
+  {
+    const int occ = kernel_occ(k_apply_moves, AM_T, AM_SMEM);
+    const i64 grid = std::max<i64>(1, std::min<i64>(cdiv(g.n, AM_CHUNK), (i64)c.sms * occ * 2));
+    LV_LAUNCH(c, k_apply_moves, (unsigned)grid, AM_T, AM_SMEM, g.n, label, a.label_next, g.delta.p, a.cpk, deg_next,
+              size_next, (int)narrow);
+  }
+  if (tm) tm->end(c.s);
   LV_LAUNCH(c, k_cpk, grid_for(c, g.n), 256, 0, g.n, deg_next, size_next, st.cpk[st.cur ^ 1].p);
   if (tm && mode == M_SWEEP) tm->end(c.s);
-  if (colored) return SweepOut();
+  if (colored || enqueue_only) return SweepOut();
   LV_CUDA(cudaMemcpyAsync(h->hctr, src, (size_t)nsum * SLOT * sizeof(u64), cudaMemcpyDeviceToHost, c.s));
   LV_CUDA(cudaStreamSynchronize(c.s));
   SweepOut o;
@@ -412,8 +509,9 @@ double kernel_alg_bytes(const std::string &nm, const Bins &B, const DGraph &g, c
   if (nm == "sweep:hub_decide") return 40.0 * (double)B.count(NSMEM);
   if (nm == "next_state_copy") return 24.0 * (double)g.n;  // deg + size: read + write
   if (nm == "pack_entries") return 16.0 * (double)g.n;
-  if (nm == "sweep_pass") {  // the whole pass: every bin + hub path + copy + packing + cpk
-    double t = 24.0 * (double)g.n + 16.0 * (double)g.n + 16.0 * (double)g.n;
+  if (nm == "apply_moves") return 16.0 * (double)g.n;  // labels cur + next 8, δ 8 per vertex
+  if (nm == "sweep_pass") {  // the whole pass: every bin + hub path + copy + packing + moves + cpk
+    double t = 24.0 * (double)g.n + 16.0 * (double)g.n + 16.0 * (double)g.n + 16.0 * (double)g.n;
     for (int b = 0; b < NSMEM; ++b) t += (double)B.edges[b] * (12.0 + wb) + 40.0 * (double)B.count(b);
     t += (double)B.edges[NSMEM] * (12.0 + wb) + 40.0 * (double)B.count(NSMEM);
     return t;
@@ -465,6 +563,80 @@ void level_consts(louvain_ctx *h, const DGraph &g, u64 &lsum, u128 &s2_inact) {
   s2_inact = ((u128)ht[3] << 64) | ht[2];
 }
 
+// Sweeps 2..max_sweeps of Algorithm 1 as ONE graph launch: a conditional WHILE node
+// whose body is a pass (tentative sweep s), the device stop test (k_alg1_test) and the
+// commit copy.  Sweep 1 has run (and been committed) on the host path.  st.cur must be
+// 0 on entry... any parity works: the body reads buffer cur and writes cur ^ 1, and
+// k_commit_copy copies cur ^ 1 back into cur, so cur is unchanged.
+int32_t one_level_dev(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, double theta, u64 lsum, u128 s2i) {
+  Ctx &c = h->c;
+  const louvain_config &cfg = h->cfg;
+  Buf<DevLoop> dl(c.A, 1);
+  DevLoop L0;
+  memset(&L0, 0, sizeof(L0));
+  L0.first = 1;
+  L0.s = 2;
+  L0.sweeps = 1;
+  LV_CUDA(cudaMemcpyAsync(dl.p, &L0, sizeof(L0), cudaMemcpyHostToDevice, c.s));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  struct Guard {
+    cudaGraph_t *g;
+    cudaGraphExec_t *e;
+    Ctx *c;
+    ~Guard() {
+      c->capturing = false;
+      if (*e) cudaGraphExecDestroy(*e);
+      if (*g) cudaGraphDestroy(*g);
+    }
+  } guard{&graph, &exec, &c};
+  LV_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle hnd;
+  LV_CUDA(cudaGraphConditionalHandleCreate(&hnd, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hnd;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  LV_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const i64 l0 = c.launches;
+  LV_CUDA(cudaStreamBeginCaptureToGraph(c.s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  c.capturing = true;
+  try {
+    run_pass(h, g, P, st, M_SWEEP, nullptr, nullptr, false, nullptr, true);
+    LV_LAUNCH(c, k_alg1_test, 1, 32, 0, h->dctr.p, NBIN, g.W, lsum, (u64)(s2i >> 64), (u64)s2i, theta,
+              cfg.stop_rule, cfg.max_sweeps, dl.p, hnd);
+    LV_LAUNCH(c, k_commit_copy, grid_for(c, g.n), 256, 0, g.n, dl.p, st.lab[st.cur].p, st.lab[st.cur ^ 1].p,
+              st.deg[st.cur].p, st.deg[st.cur ^ 1].p, st.size[st.cur].p, st.size[st.cur ^ 1].p,
+              st.cpk[st.cur].p, st.cpk[st.cur ^ 1].p);
+  } catch (...) {
+    cudaGraph_t tmp = nullptr;
+    cudaStreamEndCapture(c.s, &tmp);
+    throw;
+  }
+  cudaGraph_t tmp = nullptr;
+  LV_CUDA(cudaStreamEndCapture(c.s, &tmp));
+  c.capturing = false;
+  const i64 per_pass = c.launches - l0;  // kernels of one body (counted once by the capture)
+  LV_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  LV_CUDA(cudaGraphLaunch(exec, c.s));
+  DevLoop L;
+  LV_CUDA(cudaMemcpyAsync(&L, dl.p, sizeof(L), cudaMemcpyDeviceToHost, c.s));
+  LV_CUDA(cudaStreamSynchronize(c.s));
+  c.launches += per_pass * (L.passes - 1) + 1;  // + the graph launch itself
+  h->edge_visits += (i64)L.passes * g.nnz;
+  for (const Bins *B : P.parts)  // a bucket beyond its distinct-key capacity would have been dropped
+    if (B->nhub) {
+      int ovf = 0;
+      LV_CUDA(cudaMemcpyAsync(&ovf, B->overflow.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+      LV_CUDA(cudaStreamSynchronize(c.s));
+      LV_REQUIRE(ovf == 0, LV_ECUDA, "hub bucket overflow (a hash bucket exceeded its table)");
+    }
+  return L.sweeps;
+}
+
 // Algorithm 1 for one level.  Returns the number of committed sweeps.
 // lsum = Σ loop and s2i = Σ_{inactive} δ² of the level (of the uncompacted graph).
 int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, double theta, u64 lsum, u128 s2i) {
@@ -481,6 +653,9 @@ int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, dou
   if (prof) account(h->prof, tm, B, g, pb, o.moved);
   int32_t sweeps = 1;
   if (o.moved == 0) return sweeps;
+  // sweeps 2.. on the device (one sync per level) unless profiling / sharded / disabled
+  static const bool no_dev_loop = getenv("LV_HOST_LOOP") != nullptr;
+  if (!prof && !P.sharded && !no_dev_loop && cfg.max_sweeps >= 2) return one_level_dev(h, g, P, st, theta, lsum, s2i);
   bool first = true;
   double Qp = 0.0;
   for (int32_t s = 2; s <= cfg.max_sweeps; ++s) {
@@ -705,7 +880,9 @@ void run_impl(louvain_ctx *h) {
     }
     LV_CUDA(cudaStreamSynchronize(c.s));
     double t1 = now_ms();
-    rec->sweeps = cfg.coloring ? one_level_colored(h, gs, CP, st, theta, lsum, s2i)
+    // (the colouring path's S2 sums deg over every vertex of gs: the inactive vertices'
+    // δ² are already in it unless the compaction dropped them)
+    rec->sweeps = cfg.coloring ? one_level_colored(h, gs, CP, st, theta, lsum, compacted ? s2i : (u128)0)
                                : one_level(h, gs, P, st, theta, lsum, s2i);
     if (cfg.merge_isolated) {
       run_pass(h, gs, P, st, M_MERGE);
@@ -1051,8 +1228,8 @@ louvain_status louvain_sweep(louvain_t h, const int32_t *labels_in, int32_t *lab
     LV_CUDA(cudaMemsetAsync(st.size[0].p, 0, n * sizeof(int32_t), c.s));
     Buf<int> err(c.A, 1);
     LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
-    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, st.lab[0].p, g.delta.p, st.deg[0].p, st.size[0].p,
-              err.p);
+    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, n, st.lab[0].p, g.delta.p, st.deg[0].p,
+              st.size[0].p, err.p);
     LV_LAUNCH(c, k_cpk, grid_for(c, n), 256, 0, n, st.deg[0].p, st.size[0].p, st.cpk[0].p);
     int herr = 0;
     LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
@@ -1206,7 +1383,11 @@ louvain_status louvain_contract(louvain_t h, const int32_t *labels, int64_t k, i
     LV_CUDA(cudaMemsetAsync(nsize.p, 0, k * sizeof(int32_t), c.s));
     Buf<int> err(c.A, 1);
     LV_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.s));
-    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, lab.p, g.delta.p, ndelta.p, nsize.p, err.p);
+    LV_LAUNCH(c, k_state_from_labels, grid_for(c, n), 256, 0, n, k, lab.p, g.delta.p, ndelta.p, nsize.p, err.p);
+    int herr = 0;
+    LV_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+    LV_REQUIRE(herr == 0, LV_EINVAL, "labels must lie in [0,k)");
     Bins &B = vbins0(h);
     DGraph hg;
     contract(c, g, B, lab.p, k, std::move(ndelta), hg);

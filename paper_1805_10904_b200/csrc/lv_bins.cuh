@@ -4,31 +4,30 @@
 #pragma once
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "lv_agg.cuh"
 #include "lv_scan.cuh"
+#include "lv_sweep.cuh"
 
 namespace lv {
 
 // bin b holds rows of length in (BIN_MAX[b-1], BIN_MAX[b]]; bin NSMEM holds the hubs
-constexpr int NSMEM = 9;
+constexpr int NSMEM = 11;
 constexpr int NBIN = NSMEM + 1;
-constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 512, 2048, 4096, 8192};
+constexpr i64 BIN_MAX[NSMEM] = {4, 8, 16, 32, 128, 256, 512, 1024, 2048, 4096, 8192};
 
 __device__ __forceinline__ int bin_of(i64 d) {
+  constexpr i64 M[NSMEM] = {4, 8, 16, 32, 128, 256, 512, 1024, 2048, 4096, 8192};  // = BIN_MAX
   if (d <= 0) return 255;
-  if (d <= 4) return 0;
-  if (d <= 8) return 1;
-  if (d <= 16) return 2;
-  if (d <= 32) return 3;
-  if (d <= 128) return 4;
-  if (d <= 512) return 5;
-  if (d <= 2048) return 6;
-  if (d <= 4096) return 7;
-  if (d <= 8192) return 8;
-  return 9;
+  int b = 0;
+#pragma unroll
+  for (int i = 0; i < NSMEM; ++i) b += d > M[i];
+  return b;
 }
 
 struct KTimer {  // optional per-launch CUDA-event timing (profiling; may nest)
@@ -172,6 +171,35 @@ inline unsigned grid_for(const Ctx &c, i64 n, int per = 256) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;
+}
+
+// Resident CTAs per SM of kernel fn at (block, dynamic smem) on the CURRENT device, after
+// raising fn's dynamic shared-memory limit there if smem needs it.  Cached per (device,
+// kernel, block, smem) under a mutex: the attribute is per device, and distinct handles
+// (possibly on other devices / threads) share these caches.  The limit only ever grows,
+// so a cached smaller configuration never lowers it below a larger one in use.
+template <class F>
+inline int kernel_occ(F fn, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void *, int, size_t>, int> occ;
+  static std::map<std::pair<int, const void *>, size_t> attr;
+  int dev = 0;
+  LV_CUDA(cudaGetDevice(&dev));
+  const void *f = (const void *)fn;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, f, block, smem);
+  const auto it = occ.find(key);
+  if (it != occ.end()) return it->second;
+  size_t &cur = attr[std::make_pair(dev, f)];
+  if (smem > cur) {
+    LV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  int o = 0;
+  LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, block, smem));
+  o = o > 0 ? o : 1;
+  occ[key] = o;
+  return o;
 }
 
 // Partition rows [0,nrows) of `ptr` into length bins; set up hub tables sized for at
@@ -333,12 +361,7 @@ void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
     static const int thr_env = getenv("LV_THR") ? atoi(getenv("LV_THR")) : 8;
     if (G <= thr_env) {
       auto kt = k_sweep_thr<G, WT>;
-      static int occ_t = -1;
-      if (occ_t < 0) {
-        int o = 0;
-        LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kt, 256, 0));
-        occ_t = o > 0 ? o : 1;
-      }
+      const int occ_t = kernel_occ(kt, 256, 0);
       const i64 grid_t = std::min<i64>(cdiv(a.nrows, 256), (i64)c.sms * occ_t * 8);
       if (tm) tm->begin(st, tag);
       LV_LAUNCH_ON(c, st, kt, (unsigned)grid_t, 256, 0, a);
@@ -348,12 +371,7 @@ void launch_reg(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   }
   auto kern = (MODE == M_SWEEP && pipe) ? k_sweep_reg<G, BLOCK, WT, NARROW> : k_agg_reg<G, BLOCK, MODE, WT, NARROW>;
   constexpr int GPB = BLOCK / G;
-  static int occ = -1;
-  if (occ < 0) {
-    int o = 0;
-    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, 0));  // (per kernel choice)
-    occ = o > 0 ? o : 1;
-  }
+  const int occ = kernel_occ(kern, BLOCK, 0);
   i64 grid = cdiv(a.nrows, GPB);
   // the pipelined kernel at G = 8, 16 is persistent (one resident wave: many rows per
   // group keep the pipeline full; measured faster), otherwise up to 8 waves
@@ -370,13 +388,7 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   auto kern = k_agg_smem<G, CAP, BLOCK, MODE, WT, VT>;
   constexpr int GPB = BLOCK / G;
   const size_t smem = smem_bytes<G, CAP, BLOCK, VT, MODE>();
-  static int occ = -1;
-  if (occ < 0) {
-    LV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int o = 0;
-    LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, BLOCK, smem));
-    occ = o > 0 ? o : 1;
-  }
+  const int occ = kernel_occ(kern, BLOCK, smem);
   i64 grid = cdiv(a.nrows, GPB);
   i64 cap = (i64)c.sms * occ * 8;
   if (grid > cap) grid = cap;
@@ -385,15 +397,28 @@ void launch_bin(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   if (tm) tm->end(st);
 }
 
-static const char *BIN_NAME[NBIN] = {"reg_g4",           "reg_g8",           "reg_g16",
-                                     "reg_g32",          "agg_g32_c256",     "agg_blk128_c1024",
-                                     "agg_blk256_c4096", "agg_blk512_c8192", "agg_blk1024_c16384",
-                                     "agg_hub"};
+static const char *BIN_NAME[NBIN] = {"reg_g4",    "reg_g8",    "reg_g16",    "reg_g32",
+                                     "tab_le128", "tab_le256", "tab_le512",  "tab_le1024",
+                                     "tab_le2048", "tab_le4096", "tab_le8192", "agg_hub"};
+
+// The sweep kernel for the table bins (lv_sweep.cuh): WARPS warps per row, CAP slots.
+template <int WARPS, int CAP, class WT, int U = 4>
+void launch_tab(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStream_t st, bool s64all) {
+  using Cfg = TabCfg<WARPS, CAP>;
+  auto kern = s64all ? k_sweep_tab<WARPS, CAP, U, WT, true> : k_sweep_tab<WARPS, CAP, U, WT, false>;
+  const int occ = kernel_occ(kern, Cfg::NT, Cfg::SMEM);
+  i64 grid = cdiv(a.nrows, Cfg::GPC);
+  const i64 cap = (i64)c.sms * occ * 8;
+  if (grid > cap) grid = cap;
+  if (tm) tm->begin(st, tag);
+  LV_LAUNCH_ON(c, st, kern, (unsigned)grid, Cfg::NT, Cfg::SMEM, a);
+  if (tm) tm->end(st);
+}
 
 // One pass of MODE over every bin of B.  `a` carries the common arguments.  VT is the
 // shared-table value type (uint32_t only when every row sum is known to be < 2^32).
 template <int MODE, class WT, class VT>
-void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
+void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64all = false) {
   static const char *MN[3] = {"sweep", "merge", "emit"};
   u64 *ctr = a.counters;  // NBIN slots of 8 counters (one per bin) or NULL
   auto set = [&](int b) {
@@ -432,24 +457,9 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
     hb.nfin = B.nfin;
     hb.fin_lg = B.fin_lg;
     const size_t acc_smem = hub_acc_smem<VT, MODE>(B.max_blg);
-    static size_t attr_acc = 0;
-    static size_t attr_fin = 0;
     const size_t fin_smem = hub_fin_smem<VT, MODE>(B.fin_lg);
-    if (acc_smem > attr_acc) {
-      LV_CUDA(cudaFuncSetAttribute(k_hub_acc<MODE, WT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_smem));
-      attr_acc = acc_smem;
-    }
-    if (fin_smem > attr_fin) {
-      LV_CUDA(cudaFuncSetAttribute(k_hub_fin<MODE, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem));
-      attr_fin = fin_smem;
-    }
-    static int occ_acc = -1, occ_fin = -1;
-    if (occ_acc < 0) {
-      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_acc, k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem));
-      LV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_hub_fin<MODE, VT>, HUB_FIN_T, fin_smem));
-      occ_acc = std::max(occ_acc, 1);
-      occ_fin = std::max(occ_fin, 1);
-    }
+    const int occ_acc = kernel_occ(k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem);
+    const int occ_fin = kernel_occ(k_hub_fin<MODE, VT>, HUB_FIN_T, fin_smem);
     for (size_t bi = 0; bi + 1 < B.batch_h.size(); ++bi) {  // batches of whole hub rows
       hb.h0 = B.batch_h[bi];
       hb.h1 = B.batch_h[bi + 1];
@@ -472,11 +482,33 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   }
   // bins in decreasing length; concurrent mode spreads them over the side streams
   auto st = [&](int k) { return conc ? c.side[(k + 1) % Ctx::NSIDE] : c.s; };
-  if (B.count(8)) { set(8); launch_bin<1024, 16384, 1024, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[8]).c_str(), st(1)); }
-  if (B.count(7)) { set(7); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[7]).c_str(), st(0)); }
-  if (B.count(6)) { set(6); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[6]).c_str(), st(1)); }
-  if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[5]).c_str(), st(2)); }
-  if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[4]).c_str(), st(0)); }
+  // the table bins: the sweep-specialised kernel (narrow tables), else the generic one
+  static const bool old_sweep = getenv("LV_OLD_SWEEP") != nullptr;  // A/B experiments
+  const bool tab = MODE == M_SWEEP && sizeof(VT) == 4 && !old_sweep;
+  const std::string tg = pre;
+  auto nm = [&](int b) { return tg + BIN_NAME[b]; };
+  if constexpr (MODE == M_SWEEP && sizeof(VT) == 4) {
+    if (tab) {
+      // warps per row: measured r2 (C4 level 0; 16 -> 32 warps: 1.24 -> 1.11 ms, 2 -> 4:
+      // 1.24 -> 1.02 ms, 8 -> 16 in the 4096 bin: 1.45 -> 1.49 ms)
+      if (B.count(10)) { set(10); launch_tab<32, 16384, WT>(c, tm, a, nm(10).c_str(), st(1), s64all); }
+      if (B.count(9)) { set(9); launch_tab<8, 8192, WT>(c, tm, a, nm(9).c_str(), st(0), s64all); }
+      if (B.count(8)) { set(8); launch_tab<4, 4096, WT>(c, tm, a, nm(8).c_str(), st(1), s64all); }
+      if (B.count(7)) { set(7); launch_tab<4, 2048, WT>(c, tm, a, nm(7).c_str(), st(2), s64all); }
+      if (B.count(6)) { set(6); launch_tab<1, 1024, WT>(c, tm, a, nm(6).c_str(), st(0), s64all); }
+      if (B.count(5)) { set(5); launch_tab<1, 512, WT>(c, tm, a, nm(5).c_str(), st(1), s64all); }
+      if (B.count(4)) { set(4); launch_tab<1, 256, WT>(c, tm, a, nm(4).c_str(), st(2), s64all); }
+    }
+  }
+  if (!tab) {
+    if (B.count(10)) { set(10); launch_bin<1024, 16384, 1024, MODE, WT, VT>(c, tm, a, nm(10).c_str(), st(1)); }
+    if (B.count(9)) { set(9); launch_bin<512, 8192, 512, MODE, WT, VT>(c, tm, a, nm(9).c_str(), st(0)); }
+    if (B.count(8)) { set(8); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, nm(8).c_str(), st(1)); }
+    if (B.count(7)) { set(7); launch_bin<256, 4096, 256, MODE, WT, VT>(c, tm, a, nm(7).c_str(), st(2)); }
+    if (B.count(6)) { set(6); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, nm(6).c_str(), st(0)); }
+    if (B.count(5)) { set(5); launch_bin<128, 1024, 128, MODE, WT, VT>(c, tm, a, nm(5).c_str(), st(1)); }
+    if (B.count(4)) { set(4); launch_bin<32, 256, 256, MODE, WT, VT>(c, tm, a, nm(4).c_str(), st(2)); }
+  }
   if (B.count(3)) { set(3); launch_reg<32, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[3]).c_str(), st(1)); }
   if (B.count(2)) { set(2); launch_reg<16, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[2]).c_str(), st(2)); }
   if (B.count(1)) { set(1); launch_reg<8, 256, MODE, WT, VT>(c, tm, a, (pre + BIN_NAME[1]).c_str(), st(0)); }
@@ -495,12 +527,14 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr) {
   }
 }
 
+// s64all: every score of the pass fits int64 (2W·max δ < 2^63, checked by the caller)
 template <int MODE>
-void launch_agg_wt(Ctx &c, int wt, bool narrow, const Bins &B, const AggArgs &a, KTimer *tm = nullptr) {
+void launch_agg_wt(Ctx &c, int wt, bool narrow, const Bins &B, const AggArgs &a, KTimer *tm = nullptr,
+                   bool s64all = false) {
   if (narrow) {
-    if (wt == WT_NONE) launch_agg<MODE, WNone, uint32_t>(c, B, a, tm);
-    else if (wt == WT_U32) launch_agg<MODE, WU32, uint32_t>(c, B, a, tm);
-    else launch_agg<MODE, WU64, uint32_t>(c, B, a, tm);
+    if (wt == WT_NONE) launch_agg<MODE, WNone, uint32_t>(c, B, a, tm, s64all);
+    else if (wt == WT_U32) launch_agg<MODE, WU32, uint32_t>(c, B, a, tm, s64all);
+    else launch_agg<MODE, WU64, uint32_t>(c, B, a, tm, s64all);
   } else {
     if (wt == WT_NONE) launch_agg<MODE, WNone, u64>(c, B, a, tm);
     else if (wt == WT_U32) launch_agg<MODE, WU32, u64>(c, B, a, tm);

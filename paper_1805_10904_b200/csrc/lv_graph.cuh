@@ -215,6 +215,15 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   Buf<i64> rptr(c.A, n + 1);
   exclusive_scan<i64>(c, U32AsI64{cnt.p}, n, rptr.p, true);
   const i64 rnnz = d2h_i64(c, rptr.p + n);
+  // longest raw (duplicated) row: bounds every shared-table sum of the merge below
+  u64 maxcnt = 0;
+  {
+    Buf<u64> t(c.A, 1);
+    LV_CUDA(cudaMemsetAsync(t.p, 0, sizeof(u64), c.s));
+    LV_LAUNCH(c, k_max_u64<ArrayIn<uint32_t>>, grid_for(c, n), 256, 0, ArrayIn<uint32_t>{cnt.p}, n, t.p);
+    LV_CUDA(cudaMemcpyAsync(&maxcnt, t.p, sizeof(u64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  }
   const int raw_wt = in_wt == LV_W_NONE ? WT_NONE : in_wt == LV_W_I32 ? WT_U32 : WT_U64;
   Buf<int32_t> rcol(c.A, rnnz > 0 ? rnnz : 1);
   Buf<unsigned char> rw(c.A, rnnz * (i64)wbytes(raw_wt) + 8);
@@ -240,8 +249,9 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   a.w = rw.p;
   a.out_cnt = ocnt.p;
   a.out_sum = osum.p;
-  // every shared table / hub chunk holds <= 4096 entries of weight <= max w
-  const bool narrow = hs[2] < ((u64)1 << 20);
+  // 32-bit table sums only when no row sum can reach 2^32: every entry of a row's table
+  // (and every hub bucket merge across chunks) sums at most (raw row length) x (max w)
+  const bool narrow = (unsigned __int128)hs[2] * (unsigned __int128)(maxcnt > 0 ? maxcnt : 1) < ((unsigned __int128)1 << 32);
   launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);  // count pass (out_key == NULL)
   g.row_ptr.alloc(c.A, n + 1);
   exclusive_scan<i64>(c, I64Arr{ocnt.p}, n, g.row_ptr.p, true);
@@ -388,9 +398,9 @@ void permute_t(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, cons
   one(3, k_permute<32, 256, WT>, 8, 256);
   one(4, k_permute<32, 256, WT>, 8, 256);
   one(5, k_permute<128, 128, WT>, 1, 128);
-  one(6, k_permute<256, 256, WT>, 1, 256);
-  one(7, k_permute<256, 256, WT>, 1, 256);
-  one(8, k_permute<256, 256, WT>, 1, 256);
+  one(6, k_permute<128, 128, WT>, 1, 128);
+  static_assert(NSMEM == 11, "one launch per degree bin below");
+  for (int b = 7; b < NSMEM; ++b) one(b, k_permute<256, 256, WT>, 1, 256);
   if (VB.nhub) {
     Buf<i64> hb(c.A, VB.nhub);
     LV_LAUNCH(c, k_hub_bases, grid_for(c, VB.nhub), 256, 0, VB.nhub, VB.rows.p + VB.off[NSMEM], g.row_ptr.p, lab,

@@ -175,10 +175,25 @@ def _densify(u, v):
     return len(ids), inv[: len(u)], inv[len(u):], ids
 
 
+def _weights_out(wa: np.ndarray):
+    """None when every weight is 1, int64 when all are integral, else float64 (the
+    real-weight mode of reading D28 maps them to exact fixed point in the library)."""
+    if not np.all(np.isfinite(wa)) or np.any(wa <= 0):
+        raise ValueError("weights must be finite and > 0 (P:L43)")
+    if np.all(wa == 1):
+        return None
+    wi = wa.astype(np.int64)
+    if np.all(wi == wa):
+        return wi
+    return wa.astype(np.float64)
+
+
 def parse_edge_list(text: str, default_weight=1):
     """Edge list: ``src dst [w]`` per line; ``#``/``%`` comments.
 
-    Returns (Records, original_ids).  Ids are densified; weights must be > 0."""
+    Returns (Records, original_ids).  Ids are densified (sorted order); weights must be
+    finite and > 0 — integral weights come back as int64 (exact integer path), others as
+    float64 (fixed-point real-weight path, reading D28), all-ones as None."""
     us, vs, ws = [], [], []
     for ln, line in enumerate(text.splitlines(), 1):
         t = line.strip()
@@ -194,23 +209,21 @@ def parse_edge_list(text: str, default_weight=1):
             raise ValueError(f"line {ln}: {e}") from None
         if u < 0 or v < 0:
             raise ValueError(f"line {ln}: negative id")
-        if not (w > 0):
-            raise ValueError(f"line {ln}: weight must be > 0")
+        if not (w > 0) or not np.isfinite(w):
+            raise ValueError(f"line {ln}: weight must be finite and > 0")
         us.append(u); vs.append(v); ws.append(w)
+    if not us:
+        raise ValueError("no edges")
     n, su, sv, ids = _densify(np.array(us, np.int64), np.array(vs, np.int64))
-    wa = np.array(ws, np.float64)
-    wi = wa.astype(np.int64)
-    if np.all(wi == wa) and np.all(wi == 1):
-        w_out = None
-    elif np.all(wi == wa):
-        w_out = wi
-    else:
-        raise ValueError("non-integer weights: the integer-exact path needs integer weights (DESIGN.md §8)")
-    return Records(n, su, sv, w_out, name="edgelist"), ids
+    return Records(n, su, sv, _weights_out(np.array(ws, np.float64)), name="edgelist"), ids
 
 
 def parse_matrix_market(text: str):
-    """MatrixMarket coordinate (pattern|integer|real, symmetric|general)."""
+    """MatrixMarket coordinate (pattern|integer|real, symmetric|general).
+
+    Ids are 1-based in the file and kept (n = max(rows, cols)); weights as in
+    parse_edge_list.  'general' files may list (i,j) and (j,i): the library sums
+    duplicate undirected pairs (reading D25)."""
     lines = text.splitlines()
     if not lines or not lines[0].startswith("%%MatrixMarket"):
         raise ValueError("missing MatrixMarket header")
@@ -219,18 +232,19 @@ def parse_matrix_market(text: str):
             or h[4] not in ("symmetric", "general"):
         raise ValueError("unsupported MatrixMarket format")
     body = [ln for ln in lines[1:] if ln.strip() and not ln.startswith("%")]
+    if not body:
+        raise ValueError("missing size line")
     nr, nc, nz = (int(x) for x in body[0].split()[:3])
+    if len(body) - 1 < nz:
+        raise ValueError(f"expected {nz} entries, found {len(body) - 1}")
     us, vs, ws = [], [], []
     for ln in body[1:1 + nz]:
         f = ln.split()
-        us.append(int(f[0]) - 1); vs.append(int(f[1]) - 1)
+        i, j = int(f[0]) - 1, int(f[1]) - 1
+        if not (0 <= i < nr and 0 <= j < nc):
+            raise ValueError(f"entry ({i + 1},{j + 1}) outside {nr}x{nc}")
+        us.append(i); vs.append(j)
         ws.append(1.0 if h[3] == "pattern" else float(f[2]))
-    u, v, w = np.array(us, np.int64), np.array(vs, np.int64), np.array(ws)
-    if np.any(w <= 0):
-        raise ValueError("weight must be > 0")
-    if np.any(w != np.round(w)):
-        raise ValueError("non-integer weights: the integer-exact path needs integer weights")
     n = max(nr, nc)
-    w_out = None if np.all(w == 1) else w.astype(np.int64)
-    # 'general': (i,j) and (j,i) are the same undirected pair -> the library sums them
-    return Records(n, u.astype(np.int32), v.astype(np.int32), w_out, name="matrixmarket")
+    return Records(n, np.array(us, np.int32), np.array(vs, np.int32), _weights_out(np.array(ws, np.float64)),
+                   name="matrixmarket")

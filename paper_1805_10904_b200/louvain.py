@@ -123,6 +123,9 @@ class Louvain:
                 self._keep.append(ww)
                 g.w = ww.data_ptr()
                 g.wtype = kinds[ww.dtype]
+            # the conversions above ran on torch's current stream, while louvain_create
+            # reads the buffers on cfg.stream (or a library-owned stream): order them
+            t.cuda.current_stream(s.device).synchronize()
         else:
             s = np.ascontiguousarray(src, dtype=np.int32)
             d = np.ascontiguousarray(dst, dtype=np.int32)

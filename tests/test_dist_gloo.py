@@ -83,3 +83,41 @@ def test_gloo_sharding_host_logic(world):
     assert sum(res[0]["edges"]) == nnz
     for e in res[0]["edges"]:
         assert abs(e - nnz / world) <= maxdeg
+
+
+def _bench(*args, timeout=600):
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_PORT")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, env=env, cwd=root)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    return p.returncode, lines, p.stderr
+
+
+def test_bench_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` with no launcher spawns 2 local ranks (torchrun environment,
+    127.0.0.1 rendezvous); they meet in a gloo group, and only rank 0 prints a line."""
+    import json
+
+    rc, lines, err = _bench("--gpus", "2", "--dist-check")
+    assert rc == 0, err[-2000:]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["allmax_rank"] == 1.0
+
+
+def test_bench_reference_arm_world2_rank0_only():
+    """--impl reference under N ranks: rank 0 alone runs the oracle and prints one line."""
+    import json
+
+    rc, lines, err = _bench("--gpus", "2", "--impl", "reference", "--workload", "karate", "--steps", "2",
+                            "--warmup", "1")
+    assert rc == 0, err[-2000:]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["same_config"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
