@@ -257,6 +257,30 @@ struct Grp {
   }
 };
 
+// Sum of v over the lanes of `peers` (this lane's __match_any_sync class within `mask`,
+// the lanes executing the call), valid in every lane of the class.  __reduce_add_sync
+// with a per-lane (non-uniform) mask compiles to a loop over the classes (one
+// WARPSYNC.EXCLUSIVE + REDUX round per distinct key: ~24 rounds for a 32-entry row
+// whose keys are mostly distinct — r2 ncu, k_agg_reg<32>: 26 warp instructions per
+// edge); here every lane adds into its class leader's word of a per-warp shared buffer
+// `wb` (32 words, zero between calls), so the cost is one shared reduction per lane.
+// Lanes whose class is a singleton (the common case) skip the buffer when the whole
+// warp has no duplicate (lanes with valid = false — padding — do not count).  Exact
+// (integer adds).
+__device__ __forceinline__ uint32_t class_sum32(unsigned mask, unsigned peers, uint32_t v, uint32_t *wb,
+                                                bool valid = true) {
+  if (!__any_sync(mask, valid && (peers & (peers - 1u)) != 0u)) return v;  // no class with two lanes
+  const int leader = __ffs(peers) - 1;
+  const uint32_t a = saddr(wb + leader);
+  red_add_s32(a, v);
+  __syncwarp(mask);
+  const uint32_t t = (uint32_t)lds_i32(a);
+  __syncwarp(mask);
+  if ((int)(threadIdx.x & 31) == leader) wb[leader] = 0u;
+  __syncwarp(mask);
+  return t;
+}
+
 // Candidate: lexicographic key (S desc, label asc).  c is the packed key (label | singlet
 // bit, see "packed entries") so the singlet flag travels with it.  "None" has S = -2^127
 // (below every real score, |S| < 2^127) and c = INT32_MAX (no packed key equals it: that
@@ -751,6 +775,9 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
   const int grp = threadIdx.x / G;
   const int wl = threadIdx.x & 31;
   Acc acc;
+  __shared__ uint32_t segbuf[BLOCK / 32][32];  // class_sum32 buffers (one per warp)
+  segbuf[threadIdx.x >> 5][wl] = 0u;
+  __syncwarp();
   const u64 pf = l2_policy_first();
   const i64 stride = (i64)gridDim.x * GPB;
   i64 idx = (i64)blockIdx.x * GPB + grp;
@@ -816,7 +843,7 @@ __global__ void __launch_bounds__(BLOCK, LV_REG_MINB) k_agg_reg(AggArgs a) {
     } else {
       const unsigned peers = __match_any_sync(g.mask, k);
       lead = (__ffs(peers) - 1) == wl && k != EMPTY;
-      sum = __reduce_add_sync(peers, (uint32_t)w);
+      sum = class_sum32(g.mask, peers, (uint32_t)w, segbuf[threadIdx.x >> 5], k != EMPTY);
     }
     if (MODE == M_SWEEP) {
       constexpr int W = G < 32 ? G : 32;
@@ -886,6 +913,9 @@ __global__ void __launch_bounds__(BLOCK, LV_REGP_MINB) k_sweep_reg(AggArgs a) {
   Grp<G, BLOCK> g;
   const int wl = threadIdx.x & 31;
   Acc acc;
+  __shared__ uint32_t segbuf[BLOCK / 32][32];  // class_sum32 buffers (one per warp)
+  segbuf[threadIdx.x >> 5][wl] = 0u;
+  __syncwarp();
   const u64 pf = l2_policy_first(), pl = l2_policy_last();
   const i64 stride = (i64)gridDim.x * GPB;
   const i64 i0 = (i64)blockIdx.x * GPB + threadIdx.x / G;
@@ -948,7 +978,7 @@ __global__ void __launch_bounds__(BLOCK, LV_REGP_MINB) k_sweep_reg(AggArgs a) {
     } else {
       const unsigned peers = __match_any_sync(g.mask, k);
       lead = (__ffs(peers) - 1) == wl && k != EMPTY;
-      sum = __reduce_add_sync(peers, (uint32_t)w);
+      sum = class_sum32(g.mask, peers, (uint32_t)w, segbuf[threadIdx.x >> 5], k != EMPTY);
     }
     const bool cand = lead && k != own;
     acc.cand += cand;
@@ -1459,6 +1489,9 @@ __global__ void __launch_bounds__(AM_T) k_apply_moves(i64 n, const int32_t *__re
   int32_t *tk = (int32_t *)(sm + (size_t)AM_TS * 16);
   int32_t *tc = (int32_t *)(sm + (size_t)AM_TS * 20);  // Σ ±1
   const int lane = threadIdx.x & 31;
+  __shared__ uint32_t segbuf[AM_T / 32][32];  // class_sum32 buffers (one per warp)
+  segbuf[threadIdx.x >> 5][lane] = 0u;
+  __syncwarp();
   const uint32_t kb = saddr(tk);
   for (int s = threadIdx.x; s < AM_TS; s += AM_T) {
     tk[s] = EMPTY;
@@ -1513,11 +1546,12 @@ __global__ void __launch_bounds__(AM_T) k_apply_moves(i64 n, const int32_t *__re
         const int32_t a = av[u], b = bv[u];
         if (narrow) {
           const uint32_t dlo = (uint32_t)(d & 0xFFFF), dhi = (uint32_t)((u64)d >> 16);
+          uint32_t *wb = segbuf[threadIdx.x >> 5];
           const unsigned pt = __match_any_sync(mv, b);
-          const uint32_t tlo = __reduce_add_sync(pt, dlo), thi = __reduce_add_sync(pt, dhi);
+          const uint32_t tlo = class_sum32(mv, pt, dlo, wb), thi = class_sum32(mv, pt, dhi, wb);
           if (lane == __ffs(pt) - 1) put(b, (hb[u] & DEG_SAT) >= AM_HOT, 0, tlo, thi, __popc(pt));
           const unsigned po = __match_any_sync(mv, a);
-          const uint32_t olo = __reduce_add_sync(po, dlo), ohi = __reduce_add_sync(po, dhi);
+          const uint32_t olo = class_sum32(mv, po, dlo, wb), ohi = class_sum32(mv, po, dhi, wb);
           if (lane == __ffs(po) - 1) put(a, (ha[u] & DEG_SAT) >= AM_HOT, 1, olo, ohi, __popc(po));
         } else {  // wide graphs (rare): per-vertex atomics
           am_global(deg_next, size_next, b, (u64)d, 1);

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "lv_agg.cuh"
+#include "lv_hubcl.cuh"
 #include "lv_scan.cuh"
 #include "lv_sweep.cuh"
 
@@ -94,6 +95,13 @@ struct Bins {
   Buf<int2> fitem;
   Buf<HubPartial> part;
   Buf<int> overflow;
+  // cluster hub path (lv_hubcl.cuh): hub rows [0, ncl) of the hub bin fit a cluster of
+  // cl_cs CTAs (SWEEP with narrow tables runs them there; the pool path takes the rest);
+  // clhdr = their headers by decreasing length; cl_used: the last SWEEP pass used it
+  i64 ncl = 0, edges_cl = 0;
+  int cl_cs = 0;
+  Buf<RowHdr> clhdr;
+  mutable int cl_used = 0;
   i64 count(int b) const { return off[b + 1] - off[b]; }
   i64 active() const { return off[NBIN]; }
 };
@@ -202,6 +210,61 @@ inline int kernel_occ(F fn, int block, size_t smem) {
   return o;
 }
 
+// Cluster hub kernel (lv_hubcl.cuh): raise its shared-memory limit / allow a non-portable
+// cluster size on the current device (once per device and instantiation) and return how
+// many clusters of CS CTAs can be co-resident (0: unsupported).
+inline cudaLaunchConfig_t hcl_config(int cs, unsigned grid, cudaStream_t st, cudaLaunchAttribute *at) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(HCL_T, 1, 1);
+  cfg.dynamicSmemBytes = HCL_SMEM;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+template <int CS, class WT, bool S64ALL>
+inline int hcl_prepare() {
+  static std::mutex mu;
+  static std::map<int, int> done;  // device -> max active clusters
+  int dev = 0;
+  LV_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  const auto it = done.find(dev);
+  if (it != done.end()) return it->second;
+  auto kern = k_hub_cl<CS, WT, S64ALL>;
+  int n = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HCL_SMEM) == cudaSuccess &&
+      (CS <= 8 || cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = hcl_config(CS, CS * 148, nullptr, at);
+    if (cudaOccupancyMaxActiveClusters(&n, (const void *)kern, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();  // an unsupported size leaves a sticky-free error: clear it
+  done[dev] = n;
+  return n;
+}
+// cluster size used for the hub rows of this device.  Opt-in (LV_HUBCL=1): measured r2
+// on B200 (C4 level-0 sweep, hub rows of 8k-131k entries): 6.0 ms with 16-CTA and 3.7 ms
+// with 8-CTA clusters against 2.0 ms for the pool path (k_hub_acc + k_hub_fin) — remote
+// shared-memory CAS round trips (SASS: generic ATOM.E.CAS) serialise the inserts, ~0.04
+// inserts per cycle per SM.  LV_HUBCL_CS=8|16 forces a size; default 16 when 16-CTA
+// clusters fit, else 8.
+inline int hcl_cluster_size() {
+  static const char *on = getenv("LV_HUBCL");
+  if (!on || atoi(on) == 0) return 0;
+  static const int force = getenv("LV_HUBCL_CS") ? atoi(getenv("LV_HUBCL_CS")) : 0;
+  if (force == 16) return hcl_prepare<16, WU32, true>() > 0 ? 16 : 0;
+  if (force == 8) return hcl_prepare<8, WU32, true>() > 0 ? 8 : 0;
+  if (hcl_prepare<16, WU32, true>() > 0) return 16;
+  if (hcl_prepare<8, WU32, true>() > 0) return 8;
+  return 0;
+}
+
 // Partition rows [0,nrows) of `ptr` into length bins; set up hub tables sized for at
 // most `universe` distinct keys per row.
 // Only rows in [lo, hi) are binned (hi < 0: all rows).  rows_only: just B.rows / B.off
@@ -264,6 +327,40 @@ inline void finish_bins(Ctx &c, const i64 *ptr, i64 universe, Bins &B, const std
     LV_CUDA(cudaMemcpyAsync(beg.data(), hb.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaMemcpyAsync(len.data(), hl.p, B.nhub * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
     LV_CUDA(cudaStreamSynchronize(c.s));
+    // cluster-eligible hub rows first (stable), the pool path's giant rows last
+    B.ncl = 0;
+    B.edges_cl = 0;
+    B.cl_cs = hcl_cluster_size();
+    if (B.cl_cs) {
+      const i64 lim = hcl_max_len(B.cl_cs);
+      std::vector<int32_t> hr(B.nhub), hr2;
+      int32_t *dh = B.rows.p + B.off[NSMEM];
+      LV_CUDA(cudaMemcpyAsync(hr.data(), dh, B.nhub * sizeof(int32_t), cudaMemcpyDeviceToHost, c.s));
+      LV_CUDA(cudaStreamSynchronize(c.s));
+      std::vector<i64> beg2, len2;
+      for (int pass = 0; pass < 2; ++pass)
+        for (i64 h = 0; h < B.nhub; ++h)
+          if ((len[h] <= lim) == (pass == 0)) { hr2.push_back(hr[h]); beg2.push_back(beg[h]); len2.push_back(len[h]); }
+      for (i64 h = 0; h < B.nhub; ++h)
+        if (len2[h] <= lim) { ++B.ncl; B.edges_cl += len2[h]; }
+      beg.swap(beg2);
+      len.swap(len2);
+      LV_CUDA(cudaMemcpyAsync(dh, hr2.data(), B.nhub * sizeof(int32_t), cudaMemcpyHostToDevice, c.s));
+      if (B.ncl) {
+        std::vector<i64> ord(B.ncl);
+        for (i64 h = 0; h < B.ncl; ++h) ord[h] = h;
+        std::stable_sort(ord.begin(), ord.end(), [&](i64 x, i64 y) { return len[x] > len[y]; });
+        std::vector<RowHdr> ch(B.ncl);
+        for (i64 j = 0; j < B.ncl; ++j) {
+          ch[j].beg = beg[ord[j]];
+          ch[j].r = hr2[ord[j]];
+          ch[j].len = (int32_t)len[ord[j]];
+        }
+        B.clhdr.alloc(c.A, B.ncl);
+        LV_CUDA(cudaMemcpyAsync(B.clhdr.p, ch.data(), B.ncl * sizeof(RowHdr), cudaMemcpyHostToDevice, c.s));
+      }
+      LV_CUDA(cudaStreamSynchronize(c.s));  // host vectors go out of scope
+    }
     std::vector<i64> cfirst(B.nhub), bfirst(B.nhub), segoff;
     std::vector<int32_t> ccount(B.nhub), blg(B.nhub);
     std::vector<Chunk> ch;
@@ -322,7 +419,7 @@ inline void finish_bins(Ctx &c, const i64 *ptr, i64 universe, Bins &B, const std
     B.pool_chunks = 0;
     for (i64 h = 0; h < B.nhub; ++h) {
       const i64 hb0 = B.batch_h.back();
-      if (h > hb0 && B.h_cfirst[h + 1] - B.h_cfirst[hb0] > POOL_CHUNKS_MAX) B.batch_h.push_back(h);
+      if (h > hb0 && (h == B.ncl || B.h_cfirst[h + 1] - B.h_cfirst[hb0] > POOL_CHUNKS_MAX)) B.batch_h.push_back(h);
     }
     B.batch_h.push_back(B.nhub);
     for (size_t i = 0; i + 1 < B.batch_h.size(); ++i)
@@ -415,6 +512,32 @@ void launch_tab(Ctx &c, KTimer *tm, const AggArgs &a, const char *tag, cudaStrea
   if (tm) tm->end(st);
 }
 
+// The cluster hub kernel over hub rows [0, B.ncl) (B.clhdr, by decreasing length):
+// persistent, one cluster of B.cl_cs CTAs per resident slot.
+template <int CS, class WT, bool S64ALL>
+void launch_hcl_cs(Ctx &c, const AggArgs &a, const Bins &B, cudaStream_t st) {
+  auto kern = k_hub_cl<CS, WT, S64ALL>;
+  const int act = hcl_prepare<CS, WT, S64ALL>();
+  LV_REQUIRE(act > 0, LV_ECUDA, "cluster hub kernel cannot be resident");
+  const i64 ncl = std::min<i64>(B.ncl, act);
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = hcl_config(CS, (unsigned)(ncl * CS), st, at);
+  LV_CUDA(cudaLaunchKernelEx(&cfg, kern, a, (const RowHdr *)B.clhdr.p, B.ncl, B.overflow.p));
+  c.launches++;
+}
+template <class WT>
+void launch_hcl(Ctx &c, KTimer *tm, const AggArgs &a, const Bins &B, cudaStream_t st, bool s64all, const char *tag) {
+  if (tm) tm->begin(st, tag);
+  if (B.cl_cs == 16) {
+    if (s64all) launch_hcl_cs<16, WT, true>(c, a, B, st);
+    else launch_hcl_cs<16, WT, false>(c, a, B, st);
+  } else {
+    if (s64all) launch_hcl_cs<8, WT, true>(c, a, B, st);
+    else launch_hcl_cs<8, WT, false>(c, a, B, st);
+  }
+  if (tm) tm->end(st);
+}
+
 // One pass of MODE over every bin of B.  `a` carries the common arguments.  VT is the
 // shared-table value type (uint32_t only when every row sum is known to be < 2^32).
 template <int MODE, class WT, class VT>
@@ -460,9 +583,16 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
     const size_t fin_smem = hub_fin_smem<VT, MODE>(B.fin_lg);
     const int occ_acc = kernel_occ(k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem);
     const int occ_fin = kernel_occ(k_hub_fin<MODE, VT>, HUB_FIN_T, fin_smem);
+    // SWEEP with narrow tables: the cluster kernel takes hub rows [0, ncl)
+    const bool use_cl = MODE == M_SWEEP && sizeof(VT) == 4 && B.ncl > 0;
+    if (MODE == M_SWEEP) B.cl_used = use_cl;
+    if constexpr (MODE == M_SWEEP && sizeof(VT) == 4) {
+      if (use_cl) launch_hcl<WT>(c, tm, a, B, hub_s, s64all, (pre + "hub_cl").c_str());
+    }
     for (size_t bi = 0; bi + 1 < B.batch_h.size(); ++bi) {  // batches of whole hub rows
       hb.h0 = B.batch_h[bi];
       hb.h1 = B.batch_h[bi + 1];
+      if (use_cl && hb.h1 <= B.ncl) continue;
       hb.c0 = B.h_cfirst[hb.h0];
       hb.c1 = B.h_cfirst[hb.h1];
       hb.f0 = B.h_bfirst[hb.h0];

@@ -62,3 +62,14 @@ def test_nccl_world1_matches_oracle():
                 assert g.modularity() == want.final_q
     finally:
         lib.louvain_nccl_destroy(comm)
+
+
+@pytest.mark.parametrize("cs", ["16", "8"])
+def test_cluster_hub_path_matches_oracle(cs):
+    """The opt-in thread-block-cluster hub kernel (lv_hubcl.cuh, LV_HUBCL=1): hub rows'
+    e_{i->C} tables sharded over the cluster's shared memory — same decisions as the
+    oracle (_star_plus has a 20k-entry hub row, R-MAT 14 several)."""
+    env = dict(os.environ, LV_HUBCL="1", LV_HUBCL_CS=cs,
+               PYTHONPATH=os.pathsep.join([HERE, os.path.dirname(HERE), os.environ.get("PYTHONPATH", "")]))
+    out = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
