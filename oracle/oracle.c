@@ -253,17 +253,15 @@ int og_graph_build_real(int64_t n, int64_t m, const int32_t *src, const int32_t 
 /* Eq. 1 scratch of one thread: e_{i→c} per label, and the list of touched labels */
 typedef struct {
     int64_t *e;          /* e_{i→c} accumulator (Eq. 1)                */
-    uint8_t *mark;       /* c touched                                  */
     int32_t *touched;    /* list of touched labels                     */
 } scratch_t;
 
 static int scratch_init(scratch_t *s, int64_t n) {
     s->e = (int64_t *)calloc((size_t)n, sizeof(int64_t));
-    s->mark = (uint8_t *)calloc((size_t)n, 1);
     s->touched = (int32_t *)malloc((size_t)n * sizeof(int32_t));
-    return s->e && s->mark && s->touched;
+    return s->e && s->touched;
 }
-static void scratch_free(scratch_t *s) { free(s->e); free(s->mark); free(s->touched); }
+static void scratch_free(scratch_t *s) { free(s->e); free(s->touched); s->e = NULL; s->touched = NULL; }
 
 struct og_state {
     const og_graph *g;
@@ -273,19 +271,32 @@ struct og_state {
     scratch_t s;         /* scratch of og_decide (single-vertex calls)  */
 };
 
+/* Eq. 2: deg_C = Σ_{i∈C} δ_i (and |C|), indexed by label.  Integer sums: the parallel
+ * loop with atomic adds gives the same result as the sequential one. */
+static void community_sums(int64_t n, const int32_t *labels, const int64_t *delta, int64_t *deg, int64_t *size) {
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < n; ++c) { deg[c] = 0; if (size) size[c] = 0; }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+#pragma omp atomic
+        deg[labels[i]] += delta[i];
+        if (size) {
+#pragma omp atomic
+            size[labels[i]] += 1;
+        }
+    }
+}
+
 og_state *og_state_new(const og_graph *g, const int32_t *labels) {
     og_state *st = (og_state *)calloc(1, sizeof(og_state));
     if (!st) return NULL;
     int64_t n = g->n;
     st->g = g;
     st->C = labels;
-    st->deg = (int64_t *)calloc((size_t)n, sizeof(int64_t));
-    st->size = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    st->deg = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    st->size = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
     if (!st->deg || !st->size) { og_state_free(st); return NULL; }
-    for (int64_t i = 0; i < n; ++i) {            /* Eq. 2: deg_C = Σ_{i∈C} δ_i */
-        st->deg[labels[i]] += g->delta[i];
-        st->size[labels[i]] += 1;
-    }
+    community_sums(n, labels, g->delta, st->deg, st->size);
     return st;
 }
 
@@ -317,14 +328,14 @@ static int32_t decide(const og_state *st, scratch_t *sc, int64_t i, int32_t mode
     int64_t nt = 0;
     for (int64_t k = b; k < eend; ++k) {             /* Eq. 1 */
         int32_t c = C[g->col[k]];
-        if (!sc->mark[c]) { sc->mark[c] = 1; sc->touched[nt++] = c; }
+        if (sc->e[c] == 0) sc->touched[nt++] = c;    /* weights are > 0: e = 0 iff untouched */
         sc->e[c] += g->w[k];
     }
     int32_t result = own;
     if (mode == 0) {
         i128 twoW = (i128)2 * g->W;
         i128 di = g->delta[i];
-        int64_t e_own = sc->mark[own] ? sc->e[own] : 0;
+        int64_t e_own = sc->e[own];
         i128 S_own = twoW * e_own - di * ((i128)st->deg[own] - di);
         int32_t best = -1;
         i128 S_best = 0;
@@ -348,13 +359,27 @@ static int32_t decide(const og_state *st, scratch_t *sc, int64_t i, int32_t mode
             else result = T;
         }
     }
-    for (int64_t t = 0; t < nt; ++t) { sc->e[sc->touched[t]] = 0; sc->mark[sc->touched[t]] = 0; }
+    for (int64_t t = 0; t < nt; ++t) sc->e[sc->touched[t]] = 0;
     return result;
 }
 
 int32_t og_decide(og_state *st, int64_t i, int32_t mode) {
     if (!st->s.e && !scratch_init(&st->s, st->g->n)) return -1;
     return decide(st, &st->s, i, mode);
+}
+
+/* Per-thread Eq. 1 scratch, kept across sweeps (decide() leaves it all-zero), so a
+ * sweep does not re-allocate and re-fault n-length arrays per thread.  Grown on demand. */
+static __thread scratch_t tl_scratch;
+static __thread int64_t tl_scratch_n = 0;
+static scratch_t *thread_scratch(int64_t n) {
+    if (tl_scratch_n < n) {
+        if (tl_scratch_n) scratch_free(&tl_scratch);
+        tl_scratch_n = 0;
+        if (!scratch_init(&tl_scratch, n)) { scratch_free(&tl_scratch); return NULL; }
+        tl_scratch_n = n;
+    }
+    return &tl_scratch;
 }
 
 int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_out, int32_t mode) {
@@ -366,19 +391,17 @@ int64_t og_sweep(const og_graph *g, const int32_t *labels_in, int32_t *labels_ou
      * independent and the loop may run on any number of threads. */
 #pragma omp parallel reduction(+ : moved)
     {
-        scratch_t sc;
-        int ok = scratch_init(&sc, g->n);
-        if (!ok) {
+        scratch_t *sc = thread_scratch(g->n);
+        if (!sc) {
 #pragma omp atomic write
             err = 1;
         }
 #pragma omp for schedule(dynamic, 256)
         for (int64_t i = 0; i < g->n; ++i) {
-            if (!ok) continue;
-            labels_out[i] = decide(st, &sc, i, mode);
+            if (!sc) continue;
+            labels_out[i] = decide(st, sc, i, mode);
             moved += labels_out[i] != labels_in[i];
         }
-        scratch_free(&sc);
     }
     og_state_free(st);
     return err ? -1 : moved;
@@ -622,8 +645,7 @@ static int one_level(const og_graph *g, const og_config *cfg, double theta, int3
         if (moved < 0) { free(color); free(next); free(deg); return OG_ENOMEM; }
         *visits += g->nnz;
         memcpy(C, next, (size_t)n * sizeof(int32_t));     /* commit (D13) */
-        for (int64_t c = 0; c < n; ++c) deg[c] = 0;
-        for (int64_t i = 0; i < n; ++i) deg[C[i]] += g->delta[i];
+        community_sums(n, C, g->delta, deg, NULL);
         int64_t I2; i128 S2;
         modularity_num(g, C, deg, &I2, &S2);              /* "Compute new modularity" */
         double Q = q_from_num(g->W, I2, S2);
