@@ -106,6 +106,19 @@ typedef struct {
     int64_t color_cap_min_n; /* D29: the class cap applies only to level graphs of more than
                                 this many vertices (small dense levels keep every colour, so
                                 no synchronous class oscillates there); default 65536     */
+    int32_t reorder;         /* SURVEY F3 ("divergence ... could be reduced by ordering
+                                the vertices by degree"): 1 = relabel the vertices before the
+                                CSR build, in decreasing degree class — new id = position in
+                                the stable order of key(v) = clz(d(v)) (d(v) = non-loop records
+                                incident to v, duplicates counted; d = 0 -> key 32), i.e. by
+                                floor(log2 d) descending, ascending old id within a class.  The
+                                method then runs on the relabelled graph (the minimum-label
+                                rule sees the new ids, so partitions equal the oracle's on the
+                                same relabelled graph, not on the original one); partitions
+                                of level 0 and of level -1 are returned indexed by the
+                                ORIGINAL vertex ids; community ids, levels >= 1 and the
+                                step-level entry points (louvain_sweep, louvain_get_csr, ...)
+                                use the relabelled ids.  Default 0.                        */
 } louvain_config;
 
 /* Fill `cfg` with the defaults above. */

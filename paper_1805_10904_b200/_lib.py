@@ -62,6 +62,7 @@ class Config(C.Structure):
         ("coloring", C.c_int32),
         ("color_classes", C.c_int32),
         ("color_cap_min_n", C.c_int64),
+        ("reorder", C.c_int32),
     ]
 
 

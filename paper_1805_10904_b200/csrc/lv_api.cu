@@ -125,6 +125,35 @@ __global__ void k_compose(i64 n, int32_t *p, const int32_t *lev) {
   for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < n; i += (i64)gridDim.x * 256) p[i] = lev[p[i]];
 }
 
+// ---- F3 degree-class relabel (louvain_config.reorder)
+// d(v) = non-loop records incident to v (duplicates counted); out-of-range ids are left
+// for build_csr to reject
+__global__ void k_rec_degree(i64 m, i64 n, const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                             uint32_t *cnt) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < m; i += (i64)gridDim.x * 256) {
+    const int32_t s = src[i], d = dst[i];
+    if (s != d && s >= 0 && d >= 0 && s < n && d < n) {
+      atomicAdd(&cnt[s], 1u);
+      atomicAdd(&cnt[d], 1u);
+    }
+  }
+}
+// key(v) = clz(d(v)) = 31 - floor(log2 d) for d >= 1, 32 for d = 0
+__global__ void k_deg_key(i64 n, const uint32_t *__restrict__ cnt, uint8_t *key) {
+  for (i64 v = (i64)blockIdx.x * 256 + threadIdx.x; v < n; v += (i64)gridDim.x * 256)
+    key[v] = (uint8_t)(cnt[v] ? __clz(cnt[v]) : 32);
+}
+// perm[old] = new from the new-order list inv[new] = old
+__global__ void k_invert(i64 n, const int32_t *__restrict__ inv, int32_t *perm) {
+  for (i64 j = (i64)blockIdx.x * 256 + threadIdx.x; j < n; j += (i64)gridDim.x * 256) perm[inv[j]] = (int32_t)j;
+}
+__global__ void k_relabel(i64 m, i64 n, const int32_t *__restrict__ perm, const int32_t *__restrict__ in, int32_t *out) {
+  for (i64 i = (i64)blockIdx.x * 256 + threadIdx.x; i < m; i += (i64)gridDim.x * 256) {
+    const int32_t v = in[i];
+    out[i] = (v >= 0 && v < n) ? perm[v] : v;
+  }
+}
+
 struct LoopArr {
   const i64 *a;
   __device__ __forceinline__ u64 operator()(i64 i) const { return (u64)a[i]; }
@@ -278,6 +307,7 @@ struct louvain_ctx {
   double csr_ms = 0;
   std::vector<std::unique_ptr<LevelRec>> levels;
   Buf<int32_t> final_part;
+  Buf<int32_t> perm;           // F3 (cfg.reorder): perm[original id] = relabelled id
   bool ran = false;
   std::string err;
   i64 edge_visits = 0;
@@ -946,6 +976,13 @@ void run_impl(louvain_ctx *h) {
   LV_LAUNCH(c, k_copy_i32, grid_for(c, n0), 256, 0, n0, h->levels[0]->labels.p, h->final_part.p);
   for (size_t l = 1; l < h->levels.size(); ++l)
     LV_LAUNCH(c, k_compose, grid_for(c, n0), 256, 0, n0, h->final_part.p, h->levels[l]->labels.p);
+  if (h->perm.p) {  // F3: level-0 and final partitions indexed by the original ids
+    Buf<int32_t> t0(c.A, n0), t1(c.A, n0);
+    LV_LAUNCH(c, k_gather_i32, grid_for(c, n0), 256, 0, n0, h->perm.p, h->levels[0]->labels.p, t0.p);
+    LV_LAUNCH(c, k_gather_i32, grid_for(c, n0), 256, 0, n0, h->perm.p, h->final_part.p, t1.p);
+    LV_LAUNCH(c, k_copy_i32, grid_for(c, n0), 256, 0, n0, t0.p, h->levels[0]->labels.p);
+    LV_LAUNCH(c, k_copy_i32, grid_for(c, n0), 256, 0, n0, t1.p, h->final_part.p);
+  }
   LV_CUDA(cudaStreamSynchronize(c.s));
   h->run_launches = c.launches - l0;
   h->ran = true;
@@ -1084,6 +1121,37 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
         dw.alloc(h->c.A, gr->m * wb);
         LV_CUDA(cudaMemcpyAsync(dw.p, gr->w, gr->m * wb, cudaMemcpyHostToDevice, h->c.s));
         w = dw.p;
+      }
+    }
+    Buf<int32_t> rsrc, rdst;
+    if (cfg.reorder && gr->n > 0) {  // F3: degree-class relabel
+      Ctx &c = h->c;
+      const i64 n = gr->n, m = gr->m;
+      Buf<uint32_t> cnt(c.A, n);
+      Buf<uint8_t> key(c.A, n);
+      Buf<i64> pos(c.A, n + 1);
+      Buf<int32_t> inv(c.A, n);
+      LV_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(uint32_t), c.s));
+      if (m > 0) LV_LAUNCH(c, k_rec_degree, grid_for(c, m), 256, 0, m, n, src, dst, cnt.p);
+      LV_LAUNCH(c, k_deg_key, grid_for(c, n), 256, 0, n, cnt.p, key.p);
+      i64 off = 0;
+      for (int b = 0; b <= 32; ++b) {  // stable partition by key: ascending key, then old id
+        i64 nb = 0;
+        exclusive_scan<i64>(c, IsBin{key.p, b}, n, pos.p, true);
+        LV_CUDA(cudaMemcpyAsync(&nb, pos.p + n, sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+        LV_CUDA(cudaStreamSynchronize(c.s));
+        if (nb) LV_LAUNCH(c, k_bin_scatter, grid_for(c, n), 256, 0, n, key.p, b, pos.p, inv.p + off);
+        off += nb;
+      }
+      h->perm.alloc(c.A, n);
+      LV_LAUNCH(c, k_invert, grid_for(c, n), 256, 0, n, inv.p, h->perm.p);
+      if (m > 0) {
+        rsrc.alloc(c.A, m);
+        rdst.alloc(c.A, m);
+        LV_LAUNCH(c, k_relabel, grid_for(c, m), 256, 0, m, n, h->perm.p, src, rsrc.p);
+        LV_LAUNCH(c, k_relabel, grid_for(c, m), 256, 0, m, n, h->perm.p, dst, rdst.p);
+        src = rsrc.p;
+        dst = rdst.p;
       }
     }
     int wtype = gr->wtype;

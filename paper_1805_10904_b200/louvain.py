@@ -81,7 +81,7 @@ class Louvain:
     def __init__(self, n, src, dst, w=None, *, device=0, stream=None, torch_allocator=True,
                  theta=1e-6, big_theta=1e-6, max_sweeps=100, max_levels=64, stop_rule=0,
                  merge_isolated=True, theta_schedule=None, nccl_comm=None, rank=0, world=1, profile=False,
-                 coloring=False, color_classes=32, color_cap_min_n=65536):
+                 coloring=False, color_classes=32, color_cap_min_n=65536, reorder=False):
         self._lib = _lib.load()
         self._h = C.c_void_p()
         self._keep = []
@@ -89,7 +89,8 @@ class Louvain:
                              max_levels=int(max_levels), stop_rule=int(stop_rule),
                              merge_isolated=int(bool(merge_isolated)), device=int(device), rank=int(rank),
                              world=int(world), profile=int(bool(profile)), coloring=int(bool(coloring)),
-                             color_classes=int(color_classes), color_cap_min_n=int(color_cap_min_n))
+                             color_classes=int(color_classes), color_cap_min_n=int(color_cap_min_n),
+                             reorder=int(bool(reorder)))
         if theta_schedule:
             arr = (C.c_double * len(theta_schedule))(*[float(x) for x in theta_schedule])
             self._keep.append(arr)

@@ -19,8 +19,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="rmat24")
 ap.add_argument("--warm", type=int, default=3)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--reorder", action="store_true", help="F3 degree-class relabel (louvain_config.reorder)")
 args = ap.parse_args()
 r = inputs.make(args.workload)
-lv = Louvain(r.n, r.src, r.dst, r.w)
+lv = Louvain(r.n, r.src, r.dst, r.w, reorder=args.reorder)
 print(json.dumps(lv.time_sweeps(args.warm, args.reps)), flush=True)
 lv.close()
