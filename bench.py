@@ -73,7 +73,8 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("BENCH_CLOCK_MS", "200")], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -247,6 +248,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--dist-check", action="store_true",
                     help="launcher self-test (CPU, gloo): every rank joins, rank 0 prints world and max over ranks")
+    ap.add_argument("--library-pool", action="store_true",
+                    help="library device memory from its own stream-ordered pool (default: PyTorch's caching allocator)")
     ap.add_argument("--reorder-steps", type=int, default=1,
                     help="steps timed with the F3 degree-class relabel (reported beside the headline)")
     ap.add_argument("--coloring-steps", type=int, default=1,
@@ -296,6 +299,9 @@ def main():
     stream = torch.cuda.Stream(dev)
     torch.cuda.synchronize()
     torch.cuda.set_stream(stream)
+    # device memory of the library: PyTorch's caching allocator by default; --library-pool
+    # uses the library's own stream-ordered pool (cudaMallocAsync, release threshold raised)
+    alloc = dict(torch_allocator=not args.library_pool)
     shard = {}
     if world > 1:  # sweep-sharded (strong scaling): graph replicated, vertex ranges split
         from paper_1805_10904_b200 import dist as lvd
@@ -304,7 +310,8 @@ def main():
         shard = dict(nccl_comm=comm, rank=rank, world=world)
 
     def step(profile=False):
-        lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, profile=profile and world == 1, **shard)
+        lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, profile=profile and world == 1, **shard,
+                     **alloc)
         lv.run()
         lv.partition(-1, out=out_d)
         st = lv.run_stats()
@@ -353,7 +360,7 @@ def main():
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         with Louvain(r.n, src_h.numpy(), dst_h.numpy(), None if w_h is None else w_h.numpy(), device=local,
-                     stream=stream, **shard) as lv:
+                     stream=stream, **shard, **alloc) as lv:
             lv.run()
             host_out[:] = lv.partition(-1)
     torch.cuda.synchronize()
@@ -366,7 +373,7 @@ def main():
     coloring = None
     if args.coloring_steps > 0:
         def cstep():
-            lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, coloring=True)
+            lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, coloring=True, **alloc)
             lv.run()
             lv.partition(-1, out=out_d)
             ci = dict(q=lv.modularity(-1), sweeps=[lv.level_stats(l)[0] for l in range(lv.num_levels)],
@@ -397,7 +404,7 @@ def main():
     reorder = None
     if args.reorder_steps > 0 and world == 1:
         def rstep():
-            lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, reorder=True)
+            lv = Louvain(r.n, src_d, dst_d, w_d, device=local, stream=stream, reorder=True, **alloc)
             lv.run()
             lv.partition(-1, out=out_d)
             ri = dict(q=lv.modularity(-1), sweeps=[lv.level_stats(l)[0] for l in range(lv.num_levels)],
@@ -474,6 +481,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.workload, "graph": r.name, "n": r.n, "records": m,
+                   "allocator": "library stream-ordered pool" if args.library_pool else "torch caching allocator",
                    "directed_edges": inf["nnz"], "edge_visits_per_step": visits, "levels": inf["levels"],
                    "sweeps_per_level": inf["sweeps"], "stop_rule": "alg1_abs", "max_sweeps": 100,
                    "parallelism": f"sweep-shard{world} (graph replicated, NCCL label exchange)" if world > 1

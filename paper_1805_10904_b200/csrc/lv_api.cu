@@ -296,6 +296,38 @@ struct Prof {
   }
 };
 
+// Pinned host buffers, cached process-wide: cudaMallocHost / cudaFreeHost cost
+// milliseconds (page pinning; cudaFreeHost synchronises the device), and a handle is
+// created per graph (e.g. per bench step).  Blocks are kept and reused by size.
+struct PinnedCache {
+  std::mutex mu;
+  std::multimap<size_t, void *> free_blocks;
+  ~PinnedCache() {  // process exit: the driver may already be gone, so the blocks are left
+  }
+  void *get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.lower_bound(bytes);
+      if (it != free_blocks.end() && it->first <= 2 * bytes) {
+        void *p = it->second;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void *p = nullptr;
+    LV_CUDA(cudaMallocHost(&p, bytes));
+    return p;
+  }
+  void put(void *p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_blocks.emplace(bytes, p);
+  }
+};
+inline PinnedCache &pinned_cache() {
+  static PinnedCache *pc = new PinnedCache();  // never destroyed (see above)
+  return *pc;
+}
+
 struct louvain_ctx {
   Ctx c;
   Prof prof;
@@ -312,7 +344,8 @@ struct louvain_ctx {
   std::string err;
   i64 edge_visits = 0;
   i64 run_launches = 0;
-  u64 *hctr = nullptr;         // pinned host copy of the sweep counters
+  u64 *hctr = nullptr;         // pinned host copy of the sweep counters (pinned_cache)
+  size_t hctr_bytes = 0;
   Buf<u64> dctr;               // NBIN x 8 device counters
   std::unique_ptr<Bins> vb0;   // level-0 vertex bins (step-level API)
   // sweep-sharded mode: nccl_comm given, or LV_SHARD_SIM=P virtual ranks
@@ -331,7 +364,7 @@ struct louvain_ctx {
     dctr.release();
     g0 = DGraph();
     if (c.s) cudaStreamSynchronize(c.s);
-    if (hctr) cudaFreeHost(hctr);
+    if (hctr) pinned_cache().put(hctr, hctr_bytes);
     c.free_side();
     if (own_stream && c.s) cudaStreamDestroy(c.s);
   }
@@ -1093,7 +1126,8 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       }
     }
     const size_t nslots = (size_t)(h->world + 1) * NBIN * 8;
-    LV_CUDA(cudaMallocHost((void **)&h->hctr, nslots * sizeof(u64)));
+    h->hctr_bytes = nslots * sizeof(u64);
+    h->hctr = (u64 *)pinned_cache().get(h->hctr_bytes);
     if (const char *e = getenv("LV_L2MODE")) h->l2mode = atoi(e);
     if (h->l2mode & 4) {
       int maxp = 0, maxw = 0;
