@@ -144,18 +144,18 @@ __device__ __forceinline__ void add_u64_split(uint32_t q, u64 v) {
 template <class VT>
 __device__ __forceinline__ unsigned tab_insert(uint32_t kb, uint32_t vb, unsigned mask, int lg, int32_t k, u64 v,
                                                bool *claimed = nullptr) {
+  // CAS-first probing: one shared atomic per probe resolves all three cases — the slot is
+  // empty (claimed), holds k (found) or holds another key (next slot) — where a load
+  // followed by a CAS needed two operations and a nested branch (fewer instructions per
+  // probe in the warp-divergent probe loop)
   unsigned h = hslot(k, lg);
   while (true) {
-    const int32_t cur = lds_i32(kb + 4 * h);
-    if (cur == k) break;
-    if (cur == EMPTY) {
-      const int32_t old = cas_s32(kb + 4 * h, EMPTY, k);
-      if (old == EMPTY) {
-        if (claimed) *claimed = true;
-        break;
-      }
-      if (old == k) break;
+    const int32_t old = cas_s32(kb + 4 * h, EMPTY, k);
+    if (old == EMPTY) {
+      if (claimed) *claimed = true;
+      break;
     }
+    if (old == k) break;
     h = (h + 1) & mask;
   }
   if (sizeof(VT) == 4) red_add_s32(vb + 4 * h, (uint32_t)v);
@@ -492,10 +492,12 @@ __device__ __forceinline__ void sweep_decide(const AggArgs &a, Acc &acc, int32_t
 // Score candidate (packed key k, e_{i->C} = v, deg_C = dk) into best.
 template <bool S64>
 __device__ __forceinline__ void cand_push(Cand &best, i64 twoW, i64 di, int32_t k, u64 v, i64 dk) {
-  if (S64) {
+  if (S64) {  // branch-free select (bitwise, no short-circuit): no reconvergence per candidate
     const i64 sc = (i64)((u64)twoW * v) - (i64)((u64)di * (u64)dk);
     const i64 sb = (i64)best.lo;
-    if (sc > sb || (sc == sb && key_label(k) < key_label(best.c))) { best.lo = (u64)sc; best.c = k; }
+    const bool bt = (sc > sb) | ((sc == sb) & (key_label(k) < key_label(best.c)));
+    best.lo = bt ? (u64)sc : best.lo;
+    best.c = bt ? k : best.c;
   } else {
     const i128 S = move_score(twoW, v, di, dk);
     Cand x;

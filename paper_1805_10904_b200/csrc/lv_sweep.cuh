@@ -202,19 +202,37 @@ __global__ void __launch_bounds__(TabCfg<WARPS, CAP>::NT) k_sweep_tab(AggArgs a)
     Cand best = s64 ? cand_none64() : cand_none();
     u64 eown = 0;
     bool has_own = false;
-    for (int t = gt; t < n; t += GT) {
-      const int sl = olist[t];
-      const uint32_t d31 = odeg[t];
-      const int32_t kk = keys[sl];
-      const u64 v = vals[sl];
-      keys[sl] = EMPTY;
-      vals[sl] = 0;
-      if (kk == own) {
-        eown = v;
-        has_own = true;
-      } else {
-        if (S64ALL || s64) cand_push<true>(best, a.twoW, di, kk, v, deg_of(a, d31, key_label(kk)));
-        else cand_push<false>(best, a.twoW, di, kk, v, deg_of(a, d31, key_label(kk)));
+    if (S64ALL || s64) {  // int64 scores: predicated, one select per candidate
+      for (int t = gt; t < n; t += GT) {
+        const int sl = olist[t];
+        const uint32_t d31 = odeg[t];
+        const int32_t kk = keys[sl];
+        const u64 v = vals[sl];
+        keys[sl] = EMPTY;
+        vals[sl] = 0;
+        const bool mine = kk == own;
+        eown = mine ? v : eown;
+        has_own |= mine;
+        const i64 sc = (i64)((u64)a.twoW * v) - (i64)((u64)di * (u64)deg_of(a, d31, key_label(kk)));
+        const i64 sb = (i64)best.lo;
+        const bool bt = !mine & ((sc > sb) | ((sc == sb) & (key_label(kk) < key_label(best.c))));
+        best.lo = bt ? (u64)sc : best.lo;
+        best.c = bt ? kk : best.c;
+      }
+    } else {
+      for (int t = gt; t < n; t += GT) {
+        const int sl = olist[t];
+        const uint32_t d31 = odeg[t];
+        const int32_t kk = keys[sl];
+        const u64 v = vals[sl];
+        keys[sl] = EMPTY;
+        vals[sl] = 0;
+        if (kk == own) {
+          eown = v;
+          has_own = true;
+        } else {
+          cand_push<false>(best, a.twoW, di, kk, v, deg_of(a, d31, key_label(kk)));
+        }
       }
     }
     // e_{i->own}: at most one thread of the group met it
