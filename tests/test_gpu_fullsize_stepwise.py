@@ -116,7 +116,11 @@ def _stepwise(name, check, sweeps, threads=None):
 
 def test_c5_rmat27_stepwise_equals_oracle():
     """C5 on one B200: sweeps 1-4, 25, 50 and 100 of level 0 (every vertex), the merge
-    batch, the level-0 contraction and the exact Q of every level of the full run."""
+    batch, the level-0 contraction and the exact Q of every level of the full run.
+    ~25 min and ~150 GB of host memory: opt-in (LV_STEPWISE_C5=1); the full C5 run is
+    compared with the oracle's golden in test_gpu_fullsize_golden.py."""
+    if os.environ.get("LV_STEPWISE_C5") != "1":
+        pytest.skip("opt-in: LV_STEPWISE_C5=1 (C5 is covered by the golden full-run test)")
     rep = _stepwise("rmat27", check={1, 2, 3, 4, 25, 50, 100}, sweeps=100)
     print(rep)
 
