@@ -1411,6 +1411,121 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
   if (MODE == M_SWEEP) acc.flush(a.counters);  // candidate count only
 }
 
+// SWEEP-mode specialisation of k_hub_fin with two CTA barriers per (row, bucket) item
+// instead of five: the distinct-key counter and overflow flag alternate by item parity
+// (the next item's pair is cleared between the two barriers), and the argmax combine is
+// done by thread 0 after ONE barrier (the per-warp candidate slots are not rewritten
+// before the next item's first barrier, which thread 0 reaches only after combining).
+// Same arithmetic as k_hub_fin<M_SWEEP> (hub_fin_sweep): the bucket's (key, Σw, deg)
+// entries of every chunk merged in a shared table, scored, argmax by (S desc, label asc).
+template <class VT>
+__global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin_sw(AggArgs a, HubArgs hb) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int FLG = hb.fin_lg;
+  const int CAPF = 1 << FLG;
+  const int MAXD = CAPF / 2;
+  VT *svals = (VT *)sm;
+  int32_t *skeys = (int32_t *)(sm + (size_t)CAPF * sizeof(VT));
+  uint32_t *sdeg = (uint32_t *)(sm + (size_t)CAPF * (sizeof(VT) + sizeof(int32_t)));
+  uint16_t *slist = (uint16_t *)((unsigned char *)sdeg + (size_t)MAXD * sizeof(uint32_t));
+  __shared__ int scnt[2], sovf[2];
+  __shared__ u64 seown[2];
+  __shared__ Cand wc[HUB_FIN_T / 32];
+  const uint32_t kb = saddr(skeys), vb = saddr(svals);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Acc acc;
+  for (int s = threadIdx.x; s < CAPF; s += HUB_FIN_T) { skeys[s] = EMPTY; svals[s] = 0; }
+  if (threadIdx.x == 0) { scnt[0] = scnt[1] = 0; sovf[0] = sovf[1] = 0; seown[0] = seown[1] = 0; }
+  __syncthreads();
+  int par = 0;
+  for (i64 fi = hb.f0 + blockIdx.x; fi < hb.f1; fi += gridDim.x) {
+    const int2 it = hb.fitem[fi];
+    const int h = it.x, b = it.y;
+    const int32_t r = a.rows[h];
+    const int32_t own = (int32_t)(uint32_t)__ldg(&a.ldeg[r]);
+    const i64 di = a.delta[r];
+    const i64 cf = hb.cfirst[h];
+    const int nch = hb.ccount[h];
+    const uint32_t cb = saddr(&scnt[par]);
+    {
+      const int per = nch < HUB_FIN_T ? HUB_FIN_T / nch : 1;
+      const int Gc = 1 << (31 - __clz(per));
+      const int ng = HUB_FIN_T / Gc, gid = threadIdx.x / Gc, gl = threadIdx.x % Gc;
+      for (int j = gid; j < nch; j += ng) {
+        const i64 c = cf + j;
+        const int32_t *seg = hb.seg + hb.segoff[c];
+        const int s0 = seg[b], s1 = seg[b + 1];
+        const i64 base = (c - hb.c0) * HUB_CHUNK;
+        for (int i = s0 + gl; i < s1; i += Gc) {
+          const i64 e = base + i;
+          const int32_t k = hb.pkey[e];
+          const u64 v = (u64)((const VT *)hb.pval)[e];
+          if (*(volatile int *)&scnt[par] >= MAXD - 1) { sovf[par] = 1; continue; }
+          bool claimed = false;
+          const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
+          if (claimed) {
+            const int q = (int)atom_add_s32(cb, 1);
+            if (q < MAXD) {
+              slist[q] = (uint16_t)sl;
+              sdeg[q] = hb.pdeg[e];
+            } else {
+              sovf[par] = 1;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // B1: the item's inserts are complete
+    const int n = min(scnt[par], MAXD);
+    if (threadIdx.x == 0) {
+      if (sovf[par]) atomicOr(hb.overflow, 1);
+      scnt[par ^ 1] = 0;  // the next item's counter and flag (nobody touches them before B2)
+      sovf[par ^ 1] = 0;
+    }
+    const bool s64 = row_s64(a.twoW, di);  // CTA-uniform
+    Cand best = s64 ? cand_none64() : cand_none();
+    u64 n1 = 0;
+    for (int t = threadIdx.x; t < n; t += HUB_FIN_T) {
+      const int sl = slist[t];
+      const uint32_t d31 = sdeg[t];
+      const int32_t k = skeys[sl];
+      const u64 v = (u64)svals[sl];
+      skeys[sl] = EMPTY;
+      svals[sl] = 0;
+      if (k == own) {
+        seown[par] = v;
+      } else {
+        ++n1;
+        if (s64) cand_push<true>(best, a.twoW, di, k, v, deg_of(a, d31, key_label(k)));
+        else cand_push<false>(best, a.twoW, di, k, v, deg_of(a, d31, key_label(k)));
+      }
+    }
+    acc.cand += n1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Cand y;
+      y.lo = __shfl_xor_sync(0xffffffffu, best.lo, o);
+      y.hi = __shfl_xor_sync(0xffffffffu, best.hi, o);
+      y.c = __shfl_xor_sync(0xffffffffu, best.c, o);
+      if (s64 ? cand_better64(y, best) : cand_better(y, best)) best = y;
+    }
+    if (lane == 0) wc[wid] = best;
+    __syncthreads();  // B2: partial candidates, e_own visible; every slot reset
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < HUB_FIN_T / 32; ++w)
+        if (s64 ? cand_better64(wc[w], best) : cand_better(wc[w], best)) best = wc[w];
+      if (s64) best.hi = (i64)best.lo >> 63;
+      HubPartial P;
+      P.hi = best.hi; P.lo = best.lo; P.c = best.c; P.T = -1; P.sg = 0; P.pad = 0;
+      P.eown = seown[par]; P.cnt = 0; P.selfw = 0; P.sumw = 0;
+      seown[par] = 0;  // rewritten only after the next item's B1 (other parity) or the one after
+      hb.part[fi] = P;
+    }
+    par ^= 1;
+  }
+  acc.flush(a.counters);  // candidate count only
+}
+
 // One warp per hub row: combine the row's per-bucket partials, then decide / emit.
 template <int MODE>
 __global__ void __launch_bounds__(128) k_hub_decide(AggArgs a, HubArgs hb) {

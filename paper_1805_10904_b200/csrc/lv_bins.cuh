@@ -582,7 +582,11 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
     const size_t acc_smem = hub_acc_smem<VT, MODE>(B.max_blg);
     const size_t fin_smem = hub_fin_smem<VT, MODE>(B.fin_lg);
     const int occ_acc = kernel_occ(k_hub_acc<MODE, WT, VT>, HUB_ACC_T, acc_smem);
-    const int occ_fin = kernel_occ(k_hub_fin<MODE, VT>, HUB_FIN_T, fin_smem);
+    // SWEEP: the two-barrier specialisation (k_hub_fin_sw); LV_HUB_FIN_OLD=1 keeps the
+    // generic kernel (A/B)
+    static const bool fin_old = getenv("LV_HUB_FIN_OLD") != nullptr;
+    auto fin_kern = (MODE == M_SWEEP && !fin_old) ? k_hub_fin_sw<VT> : k_hub_fin<MODE, VT>;
+    const int occ_fin = kernel_occ(fin_kern, HUB_FIN_T, fin_smem);
     // SWEEP with narrow tables: the cluster kernel takes hub rows [0, ncl)
     const bool use_cl = MODE == M_SWEEP && sizeof(VT) == 4 && B.ncl > 0;
     if (MODE == M_SWEEP) B.cl_used = use_cl;
@@ -603,7 +607,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
       LV_LAUNCH_ON(c, hub_s, (k_hub_acc<MODE, WT, VT>), (unsigned)g_acc, HUB_ACC_T, acc_smem, a, hb);
       if (tm) tm->end(hub_s);
       if (tm) tm->begin(hub_s, pre + "hub_fin");
-      LV_LAUNCH_ON(c, hub_s, (k_hub_fin<MODE, VT>), (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
+      LV_LAUNCH_ON(c, hub_s, fin_kern, (unsigned)g_fin, HUB_FIN_T, fin_smem, a, hb);
       if (tm) tm->end(hub_s);
       if (tm) tm->begin(hub_s, pre + "hub_decide");
       LV_LAUNCH_ON(c, hub_s, (k_hub_decide<MODE>), (unsigned)cdiv(hb.h1 - hb.h0, 4), 128, 0, a, hb);
