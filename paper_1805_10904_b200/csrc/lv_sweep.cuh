@@ -73,7 +73,7 @@ struct RowStream {
 };
 
 template <int WARPS, int CAP, int U, class WT, bool S64ALL>
-__global__ void __launch_bounds__(TabCfg<WARPS, CAP>::NT) k_sweep_tab(AggArgs a) {
+__global__ void __launch_bounds__(TabCfg<WARPS, CAP>::NT, TabCfg<WARPS, CAP>::NT == 256 ? 4 : 1) k_sweep_tab(AggArgs a) {
   using Cfg = TabCfg<WARPS, CAP>;
   constexpr int GT = WARPS * 32;  // threads per group
   extern __shared__ __align__(16) unsigned char sm[];
@@ -269,17 +269,41 @@ __global__ void __launch_bounds__(TabCfg<WARPS, CAP>::NT) k_sweep_tab(AggArgs a)
         cand_k[grp][wig] = best.c;
       }
       named_bar(1 + grp, GT);  // S2: candidates and e_own visible; slots all reset
-      if (decider) {
-#pragma unroll 1
-        for (int w2 = 1; w2 < WARPS; ++w2) {
-          Cand y;
-          y.lo = cand_s[grp][w2];
-          y.hi = cand_h[grp][w2];
-          y.c = cand_k[grp][w2];
-          if (S64ALL || s64 ? cand_better64(y, best) : cand_better(y, best)) best = y;
+      if (WARPS < 8) {  // a few partials: thread 0 combines them serially
+        if (decider) {
+#pragma unroll
+          for (int w2 = 1; w2 < WARPS; ++w2) {
+            Cand y;
+            y.lo = cand_s[grp][w2];
+            y.hi = cand_h[grp][w2];
+            y.c = cand_k[grp][w2];
+            if (S64ALL || s64 ? cand_better64(y, best) : cand_better(y, best)) best = y;
+          }
+          eown = rec->eown;
+          rec->eown = 0;
         }
-        eown = rec->eown;
-        rec->eown = 0;
+      } else if (wig == 0) {  // 8-32 partials: the group's first warp combines them with
+                              // shuffles (thread 0 alone serialised the whole group behind
+                              // it at the next row's barrier: C4 le8192 bin 1.20 -> 1.02 ms)
+        Cand y = S64ALL || s64 ? cand_none64() : cand_none();
+        if (lane < WARPS) {
+          y.lo = cand_s[grp][lane];
+          y.hi = cand_h[grp][lane];
+          y.c = cand_k[grp][lane];
+        }
+#pragma unroll
+        for (int o = WARPS / 2; o > 0; o >>= 1) {
+          Cand z;
+          z.lo = __shfl_xor_sync(0xffffffffu, y.lo, o);
+          z.hi = __shfl_xor_sync(0xffffffffu, y.hi, o);
+          z.c = __shfl_xor_sync(0xffffffffu, y.c, o);
+          if (S64ALL || s64 ? cand_better64(z, y) : cand_better(z, y)) y = z;
+        }
+        best = y;
+        if (decider) {
+          eown = rec->eown;
+          rec->eown = 0;
+        }
       }
       par ^= 1;
     } else {

@@ -1,0 +1,5 @@
+#!/bin/bash
+O=gpurun_out; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -m "gpu and not slow" -x -q > $O/r2z_pytest.log 2>&1; echo "rc=$?" >> $O/r2z_pytest.log
+bash tools/variants.sh "base:LV_SO=paper_1805_10904_b200/csrc/liblouvain_base.so" "cur:" "w16:LV_TAB_W16=1" "cur2:" "w16b:LV_TAB_W16=1" > $O/r2z_variants.txt 2>&1
+echo done
