@@ -36,7 +36,7 @@ thread_local std::string g_create_error;
 typedef int (*nccl_bcast_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
 typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
 typedef int (*nccl_group_fn)();
-constexpr int NCCL_INT32 = 2, NCCL_UINT64 = 5;
+constexpr int NCCL_UINT8 = 1, NCCL_INT32 = 2, NCCL_UINT64 = 5;
 
 void *nccl_handle() {
   static void *lib = nullptr;
@@ -900,6 +900,36 @@ double q_of_contracted(louvain_ctx *h, const DGraph &hg) {
   return q_from(hg.W, (i128)2 * (i128)ht[0], (i128)(((u128)ht[3] << 64) | ht[2]));
 }
 
+// The CSR build's and the contraction's parts: sweep-sharded runs
+// split that work by row ranges; NCCL ranks compute their own part and broadcast its
+// slices, in-process simulated ranks (LV_SHARD_SIM) compute every part.
+ShardParts contract_shard(louvain_ctx *h) {
+  ShardParts S;
+  if (!h->shard || (h->world <= 1 && !h->comm)) return S;  // (a world-1 communicator still exchanges)
+  S.nparts = h->world;
+  S.mine.clear();
+  if (h->comm) {
+    S.mine.push_back(h->rank);
+    louvain_ctx *hh = h;
+    S.exchange = [hh](void *buf, size_t elem, const std::vector<i64> &off) {
+      auto bcast = nccl_sym<nccl_bcast_fn>("ncclBroadcast");
+      auto gstart = nccl_sym<nccl_group_fn>("ncclGroupStart");
+      auto gend = nccl_sym<nccl_group_fn>("ncclGroupEnd");
+      LV_NCCL(gstart());
+      for (int p = 0; p + 1 < (int)off.size(); ++p) {
+        const size_t bytes = (size_t)(off[p + 1] - off[p]) * elem;
+        if (!bytes) continue;
+        char *q = (char *)buf + (size_t)off[p] * elem;
+        LV_NCCL(bcast(q, q, bytes, NCCL_UINT8, p, hh->comm, hh->c.s));
+      }
+      LV_NCCL(gend());
+    };
+  } else {
+    for (int p = 0; p < h->world; ++p) S.mine.push_back(p);
+  }
+  return S;
+}
+
 void run_impl(louvain_ctx *h) {
   Ctx &c = h->c;
   const louvain_config &cfg = h->cfg;
@@ -983,9 +1013,9 @@ void run_impl(louvain_ctx *h) {
       gc = DGraph();
       Bins Bg;  // contraction runs on g itself
       build_bins(c, g->row_ptr.p, g->n, g->n, Bg);
-      contract(c, *g, Bg, rec->labels.p, k, std::move(ndelta), *hg);
+      contract(c, *g, Bg, rec->labels.p, k, std::move(ndelta), *hg, contract_shard(h));
     } else {
-      contract(c, *g, P.all(c, *g), rec->labels.p, k, std::move(ndelta), *hg);
+      contract(c, *g, P.all(c, *g), rec->labels.p, k, std::move(ndelta), *hg, contract_shard(h));
     }
     double t4 = now_ms();
     rec->q = q_of_contracted(h, *hg);
@@ -1195,7 +1225,7 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       w = wq.p;
       wtype = LV_W_I64;
     }
-    build_csr(h->c, gr->n, gr->m, src, dst, w, wtype, h->g0);
+    build_csr(h->c, gr->n, gr->m, src, dst, w, wtype, h->g0, contract_shard(h));
     h->csr_ms = now_ms() - t0;
   } catch (const Error &e) {
     g_create_error = e.msg;

@@ -13,6 +13,7 @@
 //                reduce_by_key): inter-community weights summed per pair, intra weight to
 //                the meta-vertex loop (old loops once; reading D19); δ' = deg_C, W' = W.
 #pragma once
+#include <functional>
 #include <cstring>
 
 #include "lv_bins.cuh"
@@ -71,17 +72,24 @@ template <class R, class WOUT>
 __global__ void __launch_bounds__(256) k_coo_fill(i64 m, const int32_t *__restrict__ src,
                                                   const int32_t *__restrict__ dst, const void *w,
                                                   const i64 *__restrict__ rptr, uint32_t *cur, int32_t *rcol,
-                                                  void *rw) {
+                                                  void *rw, int32_t lo, int32_t hi) {
+  // rows outside [lo, hi) are left empty (the sharded build's other parts)
   for (i64 k = (i64)blockIdx.x * 256 + threadIdx.x; k < m; k += (i64)gridDim.x * 256) {
     const int32_t u = src[k], v = dst[k];
     if (u == v) continue;
     const i64 wk = R::get(w, k);
-    i64 pu = rptr[u] + atomicAdd(&cur[u], 1u);
-    i64 pv = rptr[v] + atomicAdd(&cur[v], 1u);
-    rcol[pu] = v;
-    rcol[pv] = u;
-    if (WOUT::bytes == 4) { ((uint32_t *)rw)[pu] = (uint32_t)wk; ((uint32_t *)rw)[pv] = (uint32_t)wk; }
-    if (WOUT::bytes == 8) { ((u64 *)rw)[pu] = (u64)wk; ((u64 *)rw)[pv] = (u64)wk; }
+    if (u >= lo && u < hi) {
+      const i64 pu = rptr[u] + atomicAdd(&cur[u], 1u);
+      rcol[pu] = v;
+      if (WOUT::bytes == 4) ((uint32_t *)rw)[pu] = (uint32_t)wk;
+      if (WOUT::bytes == 8) ((u64 *)rw)[pu] = (u64)wk;
+    }
+    if (v >= lo && v < hi) {
+      const i64 pv = rptr[v] + atomicAdd(&cur[v], 1u);
+      rcol[pv] = u;
+      if (WOUT::bytes == 4) ((uint32_t *)rw)[pv] = (uint32_t)wk;
+      if (WOUT::bytes == 8) ((u64 *)rw)[pv] = (u64)wk;
+    }
   }
 }
 
@@ -186,10 +194,24 @@ inline int quantize_real(Ctx &c, i64 m, const void *w, int in_wt, Buf<i64> &out)
   return lo;
 }
 
+// Sharded CSR build and contraction: the rows of the graph being
+// built (level-0 vertices / the next level's communities) are split into nparts contiguous
+// ranges balanced by their raw entry counts; part p fills and aggregates only its rows.  A process computes the parts in `mine` (all of them
+// for in-process simulated ranks, its own rank with NCCL) and `exchange` (NCCL) then
+// broadcasts each part's slices from the rank that computed it — so every rank ends with
+// the whole (replicated) next-level graph while the gather + hash aggregation work is
+// split.  nparts = 1: the whole graph in one part.
+struct ShardParts {
+  int nparts = 1;
+  std::vector<int> mine{0};
+  // exchange(buf, elem_bytes, off): slice p = elements [off[p], off[p+1]) of buf, from rank p
+  std::function<void(void *, size_t, const std::vector<i64> &)> exchange;
+};
+
 // Build the level-0 CSR from device COO records.  Returns LV_OK / LV_EGRAPH / LV_EZEROW
 // through exceptions.  in_wt: 0 none, 1 int32, 2 int64 (louvain_wtype).
 inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *dst, const void *w, int in_wt,
-                      DGraph &g) {
+                      DGraph &g, const ShardParts &S = ShardParts()) {
   g.n = n;
   g.loop.alloc(c.A, n);
   g.delta.alloc(c.A, n);
@@ -225,19 +247,36 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
     LV_CUDA(cudaStreamSynchronize(c.s));
   }
   const int raw_wt = in_wt == LV_W_NONE ? WT_NONE : in_wt == LV_W_I32 ? WT_U32 : WT_U64;
+  // row parts (sharded build): balanced by raw entries; this process fills the rows of its
+  // parts ([rlo, rhi) = their union, contiguous: all parts in-process, or one rank's)
+  const int P = S.nparts;
+  std::vector<i64> rb(P + 1, 0);
+  rb[P] = n;
+  if (P > 1) {
+    Buf<i64> db(c.A, P + 1);
+    LV_LAUNCH(c, k_shard_bounds, 1, 1024, 0, n, rptr.p, P, db.p);
+    LV_CUDA(cudaMemcpyAsync(rb.data(), db.p, (P + 1) * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  }
+  i64 rlo = n, rhi = 0;
+  for (int p : S.mine) { rlo = std::min(rlo, rb[p]); rhi = std::max(rhi, rb[p + 1]); }
   Buf<int32_t> rcol(c.A, rnnz > 0 ? rnnz : 1);
   Buf<unsigned char> rw(c.A, rnnz * (i64)wbytes(raw_wt) + 8);
   LV_CUDA(cudaMemsetAsync(cnt.p, 0, n * sizeof(uint32_t), c.s));
   if (m > 0) {
-    if (in_wt == LV_W_NONE) LV_LAUNCH(c, (k_coo_fill<RNone, WNone>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
-    else if (in_wt == LV_W_I32) LV_LAUNCH(c, (k_coo_fill<RI32, WU32>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
-    else LV_LAUNCH(c, (k_coo_fill<RI64, WU64>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p);
+    const int32_t flo = (int32_t)rlo, fhi = (int32_t)rhi;
+    if (in_wt == LV_W_NONE) LV_LAUNCH(c, (k_coo_fill<RNone, WNone>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p, flo, fhi);
+    else if (in_wt == LV_W_I32) LV_LAUNCH(c, (k_coo_fill<RI32, WU32>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p, flo, fhi);
+    else LV_LAUNCH(c, (k_coo_fill<RI64, WU64>), gm, 256, 0, m, src, dst, w, rptr.p, cnt.p, rcol.p, (void *)rw.p, flo, fhi);
   }
   cnt.release();
   // merge duplicates per row (hash aggregation, emit mode), two passes: count the distinct
   // entries of every row, then write them straight into the final CSR (no temporaries)
-  Bins B;
-  build_bins(c, rptr.p, n, n, B);
+  std::vector<std::unique_ptr<Bins>> BP(P);
+  for (int p : S.mine) {
+    BP[p] = std::make_unique<Bins>();
+    build_bins(c, rptr.p, n, n, *BP[p], rb[p], rb[p + 1]);
+  }
   Buf<i64> ocnt(c.A, n);
   Buf<u64> osum(c.A, n);
   LV_CUDA(cudaMemsetAsync(ocnt.p, 0, n * sizeof(i64), c.s));
@@ -252,7 +291,11 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   // 32-bit table sums only when no row sum can reach 2^32: every entry of a row's table
   // (and every hub bucket merge across chunks) sums at most (raw row length) x (max w)
   const bool narrow = (unsigned __int128)hs[2] * (unsigned __int128)(maxcnt > 0 ? maxcnt : 1) < ((unsigned __int128)1 << 32);
-  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);  // count pass (out_key == NULL)
+  for (int p : S.mine) launch_agg_wt<M_EMIT>(c, raw_wt, narrow, *BP[p], a);  // count pass (out_key == NULL)
+  if (S.exchange) {  // every part's distinct counts and row sums (δ) from the rank that has them
+    S.exchange(ocnt.p, sizeof(i64), rb);
+    S.exchange(osum.p, sizeof(u64), rb);
+  }
   g.row_ptr.alloc(c.A, n + 1);
   exclusive_scan<i64>(c, I64Arr{ocnt.p}, n, g.row_ptr.p, true);
   g.nnz = d2h_i64(c, g.row_ptr.p + n);
@@ -275,7 +318,13 @@ inline void build_csr(Ctx &c, i64 n, i64 m, const int32_t *src, const int32_t *d
   a.out_w = g.w.p;
   a.out_w32 = g.wt == WT_U32;
   a.out_wnone = g.wt == WT_NONE;
-  launch_agg_wt<M_EMIT>(c, raw_wt, narrow, B, a);  // write pass
+  for (int p : S.mine) launch_agg_wt<M_EMIT>(c, raw_wt, narrow, *BP[p], a);  // write pass
+  if (S.exchange) {  // every part's rows
+    std::vector<i64> ro(P + 1);
+    for (int p = 0; p <= P; ++p) ro[p] = d2h_i64(c, g.row_ptr.p + rb[p]);
+    S.exchange(g.col.p, sizeof(int32_t), ro);
+    if (wbytes(g.wt)) S.exchange(g.w.p, wbytes(g.wt), ro);
+  }
   rcol.release();
   rw.release();
   LV_LAUNCH(c, k_delta, grid_for(c, n), 256, 0, n, osum.p, g.loop.p, g.delta.p);
@@ -329,15 +378,17 @@ template <int G, int BLOCK, class WT>
 __global__ void __launch_bounds__(BLOCK) k_permute(const int32_t *__restrict__ rows, i64 nrows,
                                                    const i64 *__restrict__ rp, const int32_t *__restrict__ col,
                                                    const void *w, const int32_t *__restrict__ lab,
-                                                   const i64 *__restrict__ cptr, u64 *ecur, int32_t *pk, void *pw) {
+                                                   const i64 *__restrict__ cptr, u64 *ecur, int32_t *pk, void *pw,
+                                                   int32_t clo, int32_t chi) {
   constexpr int GPB = BLOCK / G;
   __shared__ i64 sbase[GPB];
   const int grp = threadIdx.x / G, lane = threadIdx.x % G;
   const unsigned mask = G >= 32 ? 0xffffffffu : (((1u << (G & 31)) - 1u) << (((threadIdx.x & 31) / G) * G));
   for (i64 idx = (i64)blockIdx.x * GPB + grp; idx < nrows; idx += (i64)gridDim.x * GPB) {
     const int32_t v = rows[idx];
-    const i64 b = rp[v], d = rp[v + 1] - b;
     const int32_t c = lab[v];
+    if (c < clo || c >= chi) continue;  // group-uniform: another part's community (sharded contraction)
+    const i64 b = rp[v], d = rp[v + 1] - b;
     i64 base = 0;
     if (lane == 0) base = cptr[c] + (i64)atomicAdd(&ecur[c], (u64)d);
     if (G <= 32) {
@@ -360,9 +411,11 @@ template <class WT>
 __global__ void __launch_bounds__(256) k_permute_hub(const Chunk *__restrict__ chunks, const int32_t *__restrict__ rows,
                                                      const i64 *__restrict__ rp, const int32_t *__restrict__ col,
                                                      const void *w, const int32_t *__restrict__ lab,
-                                                     const i64 *__restrict__ hub_base, int32_t *pk, void *pw) {
+                                                     const i64 *__restrict__ hub_base, int32_t *pk, void *pw,
+                                                     int32_t clo, int32_t chi) {
   const Chunk ch = chunks[blockIdx.x];
   const int32_t v = rows[ch.h];
+  if (lab[v] < clo || lab[v] >= chi) return;  // CTA-uniform
   const i64 b = rp[v], base = hub_base[ch.h];
   for (i64 e = ch.beg + threadIdx.x; e < ch.end; e += 256) {
     const i64 t = e - b;
@@ -373,24 +426,28 @@ __global__ void __launch_bounds__(256) k_permute_hub(const Chunk *__restrict__ c
 }
 
 __global__ void k_hub_bases(i64 nhub, const int32_t *__restrict__ rows, const i64 *__restrict__ rp,
-                            const int32_t *__restrict__ lab, const i64 *__restrict__ cptr, u64 *ecur, i64 *hub_base) {
+                            const int32_t *__restrict__ lab, const i64 *__restrict__ cptr, u64 *ecur, i64 *hub_base,
+                            int32_t clo, int32_t chi) {
   for (i64 h = (i64)blockIdx.x * 256 + threadIdx.x; h < nhub; h += (i64)gridDim.x * 256) {
     const int32_t v = rows[h];
     const i64 d = rp[v + 1] - rp[v];
     const int32_t c = lab[v];
+    if (c < clo || c >= chi) continue;
     hub_base[h] = cptr[c] + (i64)atomicAdd(&ecur[c], (u64)d);
   }
 }
 
+// Rows of vertices whose community lies in [clo, chi) only (a part of the sharded
+// contraction; [0, k) = all).
 template <class WT>
 void permute_t(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, const i64 *cptr, u64 *ecur, int32_t *pk,
-               void *pw) {
+               void *pw, int32_t clo, int32_t chi) {
   auto one = [&](int b, auto kern, int GPB, int BLOCK) {
     if (!VB.count(b)) return;
     i64 grid = cdiv(VB.count(b), GPB);
     if (grid > (i64)c.sms * 16) grid = (i64)c.sms * 16;
     LV_LAUNCH(c, kern, (unsigned)grid, BLOCK, 0, VB.rows.p + VB.off[b], VB.count(b), g.row_ptr.p, g.col.p,
-              (const void *)g.w.p, lab, cptr, ecur, pk, pw);
+              (const void *)g.w.p, lab, cptr, ecur, pk, pw, clo, chi);
   };
   one(0, k_permute<4, 256, WT>, 64, 256);
   one(1, k_permute<8, 256, WT>, 32, 256);
@@ -404,9 +461,9 @@ void permute_t(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, cons
   if (VB.nhub) {
     Buf<i64> hb(c.A, VB.nhub);
     LV_LAUNCH(c, k_hub_bases, grid_for(c, VB.nhub), 256, 0, VB.nhub, VB.rows.p + VB.off[NSMEM], g.row_ptr.p, lab,
-              cptr, ecur, hb.p);
+              cptr, ecur, hb.p, clo, chi);
     LV_LAUNCH(c, k_permute_hub<WT>, (unsigned)VB.nchunks, 256, 0, VB.chunks.p, VB.rows.p + VB.off[NSMEM], g.row_ptr.p,
-              g.col.p, (const void *)g.w.p, lab, hb.p, pk, pw);
+              g.col.p, (const void *)g.w.p, lab, hb.p, pk, pw, clo, chi);
   }
 }
 
@@ -418,7 +475,7 @@ __global__ void k_finish_loop(i64 k, const i64 *__restrict__ nloop, const u64 *_
 // Contract g by dense labels lab (values in [0,k)); ndelta = deg of each community.
 // VB = vertex bins of g (reused from the sweeps).
 inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab, i64 k, Buf<i64> &&ndelta,
-                     DGraph &h) {
+                     DGraph &h, const ShardParts &S = ShardParts()) {
   const i64 n = g.n;
   Buf<i64> ecnt(c.A, k + 1), nloop(c.A, k);
   LV_CUDA(cudaMemsetAsync(ecnt.p, 0, (k + 1) * sizeof(i64), c.s));
@@ -426,17 +483,33 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   LV_LAUNCH(c, k_comm_edges, grid_for(c, n), 256, 0, n, lab, g.row_ptr.p, g.loop.p, ecnt.p, nloop.p);
   Buf<i64> cptr(c.A, k + 1);
   exclusive_scan<i64>(c, I64Arr{ecnt.p}, k, cptr.p, true);
+  // part boundaries over the communities
+  const int P = S.nparts;
+  std::vector<i64> cb(P + 1, 0);
+  cb[P] = k;
+  if (P > 1) {
+    Buf<i64> db(c.A, P + 1);
+    LV_LAUNCH(c, k_shard_bounds, 1, 1024, 0, k, cptr.p, P, db.p);
+    LV_CUDA(cudaMemcpyAsync(cb.data(), db.p, (P + 1) * sizeof(i64), cudaMemcpyDeviceToHost, c.s));
+    LV_CUDA(cudaStreamSynchronize(c.s));
+  }
   const i64 tot = g.nnz;
   Buf<int32_t> pk(c.A, tot > 0 ? tot : 1);
   Buf<unsigned char> pw(c.A, tot * (i64)wbytes(g.wt) + 8);
   LV_CUDA(cudaMemsetAsync(ecnt.p, 0, (k + 1) * sizeof(i64), c.s));  // reuse as cursor
-  if (g.wt == WT_NONE) permute_t<WNone>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
-  else if (g.wt == WT_U32) permute_t<WU32>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
-  else permute_t<WU64>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p);
+  for (int p : S.mine) {
+    const int32_t clo = (int32_t)cb[p], chi = (int32_t)cb[p + 1];
+    if (g.wt == WT_NONE) permute_t<WNone>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p, clo, chi);
+    else if (g.wt == WT_U32) permute_t<WU32>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p, clo, chi);
+    else permute_t<WU64>(c, g, VB, lab, cptr.p, (u64 *)ecnt.p, pk.p, pw.p, clo, chi);
+  }
   ecnt.release();
   // aggregate each community's range: count pass, then write straight into the new CSR
-  Bins CB;
-  build_bins(c, cptr.p, k, k, CB);
+  std::vector<std::unique_ptr<Bins>> CB(P);
+  for (int p : S.mine) {
+    CB[p] = std::make_unique<Bins>();
+    build_bins(c, cptr.p, k, k, *CB[p], cb[p], cb[p + 1]);
+  }
   Buf<i64> ocnt(c.A, k);
   Buf<u64> oself(c.A, k);
   LV_CUDA(cudaMemsetAsync(ocnt.p, 0, k * sizeof(i64), c.s));
@@ -451,7 +524,11 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   // a community's row sum is at most its deg_C
   const i64 maxdeg = max_of(c, ndelta.p, k);
   const bool narrow = maxdeg < ((i64)1 << 32);
-  launch_agg_wt<M_EMIT>(c, g.wt, narrow, CB, a);  // count pass (out_key == NULL)
+  for (int p : S.mine) launch_agg_wt<M_EMIT>(c, g.wt, narrow, *CB[p], a);  // count pass (out_key == NULL)
+  if (S.exchange) {
+    S.exchange(ocnt.p, sizeof(i64), cb);
+    S.exchange(oself.p, sizeof(u64), cb);
+  }
   h.n = k;
   h.W = g.W;
   h.row_ptr.alloc(c.A, k + 1);
@@ -465,7 +542,13 @@ inline void contract(Ctx &c, const DGraph &g, const Bins &VB, const int32_t *lab
   a.out_w = h.w.p;
   a.out_w32 = h.wt == WT_U32;
   a.out_wnone = 0;
-  launch_agg_wt<M_EMIT>(c, g.wt, narrow, CB, a);  // write pass
+  for (int p : S.mine) launch_agg_wt<M_EMIT>(c, g.wt, narrow, *CB[p], a);  // write pass
+  if (S.exchange) {  // every part's rows from the rank that computed them
+    std::vector<i64> ro(P + 1);
+    for (int p = 0; p <= P; ++p) ro[p] = d2h_i64(c, h.row_ptr.p + cb[p]);
+    S.exchange(h.col.p, sizeof(int32_t), ro);
+    S.exchange(h.w.p, wbytes(h.wt), ro);
+  }
   pk.release();
   pw.release();
   h.loop.alloc(c.A, k);

@@ -1,7 +1,8 @@
 """Sweep-sharded path on one GPU.
 
 The partition (edge-balanced vertex ranges, per-range bins, exact counter combination,
-replicated move application) runs with P virtual ranks in one process (LV_SHARD_SIM=P);
+replicated move application, the CSR build and the contraction computed in row parts —
+SURVEY F4) runs with P virtual ranks in one process (LV_SHARD_SIM=P);
 the NCCL exchange runs over a real world-1 NCCL communicator.  Jacobi semantics make the
 result independent of the rank count, so every configuration must equal the oracle.
 """
@@ -21,10 +22,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 CODE = """
 import numpy as np, oracle
-from test_gpu_parity import _star_plus
+from test_gpu_parity import _star_plus, _canon_fast
 from paper_1805_10904_b200 import Louvain, inputs
 for r in (inputs.karate(), inputs.rmat(14, 16, seed=3), _star_plus(seed=1), inputs.sbm(20000, 20, 32, 0.3, seed=2)):
     og = oracle.Graph.from_edges(r.n, r.src, r.dst, r.w)
+    # the CSR built in row parts (sharded build) and the level-0 contraction in community
+    # parts equal the oracle's
+    b = og.arrays()
+    with Louvain(r.n, r.src, r.dst, r.w) as g:
+        a = g.csr()
+        assert a["W"] == b["W"] and np.array_equal(a["row_ptr"], b["row_ptr"]), r.name
+        assert np.array_equal(a["loop"], b["loop"]) and np.array_equal(a["delta"], b["delta"]), r.name
+        ca, wa = _canon_fast(a["row_ptr"], a["col"], a["w"])
+        assert np.array_equal(ca, b["col"]) and np.array_equal(wa, b["w"]), r.name
     for rule in (0, 1):
         want = oracle.run(og, stop_rule=rule)
         with Louvain(r.n, r.src, r.dst, r.w, stop_rule=rule) as g:
