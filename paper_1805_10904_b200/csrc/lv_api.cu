@@ -718,7 +718,22 @@ int32_t one_level(louvain_ctx *h, const DGraph &g, const Plan &P, State &st, dou
   if (o.moved == 0) return sweeps;
   // sweeps 2.. on the device (one sync per level) unless profiling / sharded / disabled
   static const bool no_dev_loop = getenv("LV_HOST_LOOP") != nullptr;
-  if (!prof && !P.sharded && !no_dev_loop && cfg.max_sweeps >= 2) return one_level_dev(h, g, P, st, theta, lsum, s2i);
+  if (!prof && !P.sharded && !no_dev_loop && cfg.max_sweeps >= 2) {
+    // small level graphs are launch/latency-bound: their bin kernels run as parallel
+    // branches of the level's graph (side streams; C4 level 2, 13M entries: 26.8 -> 21.9 ms
+    // per 100 sweeps), large ones serially (concurrent bins measured slower there:
+    // C4 level 0 843 -> 906 ms).  LV_CONC_NNZ overrides the entry threshold.
+    static const i64 conc_nnz = getenv("LV_CONC_NNZ") ? atoll(getenv("LV_CONC_NNZ")) : ((i64)1 << 25);
+    Ctx &c = h->c;
+    const bool was = c.concurrent;
+    if (c.side[0] && !was) c.concurrent = g.nnz <= conc_nnz;
+    struct Restore {
+      Ctx &c;
+      bool v;
+      ~Restore() { c.concurrent = v; }
+    } restore{c, was};
+    return one_level_dev(h, g, P, st, theta, lsum, s2i);
+  }
   bool first = true;
   double Qp = 0.0;
   for (int32_t s = 2; s <= cfg.max_sweeps; ++s) {
@@ -1129,7 +1144,12 @@ louvain_status louvain_create(const louvain_graph *gr, const louvain_config *cfg
       LV_CUDA(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
       h->own_stream = true;
     }
-    if (getenv("LV_CONCURRENT")) h->c.init_side();
+    // side streams: LV_CONCURRENT=1 runs every pass's bins concurrently; otherwise they
+    // serve the small levels' device loops only (one_level)
+    if (!getenv("LV_NO_SIDE")) {
+      h->c.init_side();
+      if (!getenv("LV_CONCURRENT")) h->c.concurrent = false;
+    }
     if (getenv("LV_NO_COMPACT")) h->compact = false;  // degree bins on side streams (measured slower)
     if (!cfg.alloc) {  // keep freed blocks in the stream-ordered pool (no release on sync)
       cudaMemPool_t pool;
