@@ -281,6 +281,22 @@ __device__ __forceinline__ uint32_t class_sum32(unsigned mask, unsigned peers, u
   return t;
 }
 
+// Two class sums at once (one vote, one set of warp barriers): wb holds 64 words (the
+// second sum uses wb + 32).
+__device__ __forceinline__ void class_sum32x2(unsigned mask, unsigned peers, uint32_t &x, uint32_t &y, uint32_t *wb) {
+  if (!__any_sync(mask, (peers & (peers - 1u)) != 0u)) return;  // no class with two lanes
+  const int leader = __ffs(peers) - 1;
+  const uint32_t a0 = saddr(wb + leader), a1 = saddr(wb + 32 + leader);
+  red_add_s32(a0, x);
+  red_add_s32(a1, y);
+  __syncwarp(mask);
+  x = (uint32_t)lds_i32(a0);
+  y = (uint32_t)lds_i32(a1);
+  __syncwarp(mask);
+  if ((int)(threadIdx.x & 31) == leader) { wb[leader] = 0u; wb[32 + leader] = 0u; }
+  __syncwarp(mask);
+}
+
 // Candidate: lexicographic key (S desc, label asc).  c is the packed key (label | singlet
 // bit, see "packed entries") so the singlet flag travels with it.  "None" has S = -2^127
 // (below every real score, |S| < 2^127) and c = INT32_MAX (no packed key equals it: that
@@ -1606,8 +1622,9 @@ __global__ void __launch_bounds__(AM_T) k_apply_moves(i64 n, const int32_t *__re
   int32_t *tk = (int32_t *)(sm + (size_t)AM_TS * 16);
   int32_t *tc = (int32_t *)(sm + (size_t)AM_TS * 20);  // Σ ±1
   const int lane = threadIdx.x & 31;
-  __shared__ uint32_t segbuf[AM_T / 32][32];  // class_sum32 buffers (one per warp)
+  __shared__ uint32_t segbuf[AM_T / 32][64];  // class_sum32x2 buffers (one pair per warp)
   segbuf[threadIdx.x >> 5][lane] = 0u;
+  segbuf[threadIdx.x >> 5][32 + lane] = 0u;
   __syncwarp();
   const uint32_t kb = saddr(tk);
   for (int s = threadIdx.x; s < AM_TS; s += AM_T) {
@@ -1665,10 +1682,12 @@ __global__ void __launch_bounds__(AM_T) k_apply_moves(i64 n, const int32_t *__re
           const uint32_t dlo = (uint32_t)(d & 0xFFFF), dhi = (uint32_t)((u64)d >> 16);
           uint32_t *wb = segbuf[threadIdx.x >> 5];
           const unsigned pt = __match_any_sync(mv, b);
-          const uint32_t tlo = class_sum32(mv, pt, dlo, wb), thi = class_sum32(mv, pt, dhi, wb);
+          uint32_t tlo = dlo, thi = dhi;
+          class_sum32x2(mv, pt, tlo, thi, wb);
           if (lane == __ffs(pt) - 1) put(b, (hb[u] & DEG_SAT) >= AM_HOT, 0, tlo, thi, __popc(pt));
           const unsigned po = __match_any_sync(mv, a);
-          const uint32_t olo = class_sum32(mv, po, dlo, wb), ohi = class_sum32(mv, po, dhi, wb);
+          uint32_t olo = dlo, ohi = dhi;
+          class_sum32x2(mv, po, olo, ohi, wb);
           if (lane == __ffs(po) - 1) put(a, (ha[u] & DEG_SAT) >= AM_HOT, 1, olo, ohi, __popc(po));
         } else {  // wide graphs (rare): per-vertex atomics
           am_global(deg_next, size_next, b, (u64)d, 1);
