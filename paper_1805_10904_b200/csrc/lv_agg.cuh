@@ -1143,9 +1143,10 @@ struct HubArgs {
   const i64 *bfirst;      // per hub: first fin item (one per bucket)
   const i64 *segoff;      // per chunk: offset of its segment table (nb + 1 entries)
   int32_t *seg;           // segment boundaries, relative to the chunk's pool region
-  int32_t *pkey;          // pool: chunk c of this batch owns [(c - c0) * HUB_CHUNK, +HUB_CHUNK)
-  void *pval;             // pool values: uint32 when VT is 32-bit, else u64
-  uint32_t *pdeg;         // pool: deg_C (31-bit) of each entry (SWEEP/MERGE)
+  uint4 *pent;            // pool: chunk c of this batch owns [(c - c0) * HUB_CHUNK, +HUB_CHUNK);
+                          //   entries packed {key, deg_C (SWEEP/MERGE), Σw lo, Σw hi} — ONE
+                          //   16-byte store / load per entry (not three scattered 4-8 byte
+                          //   accesses to separate key / value / degree arrays)
   i64 c0, c1;            // chunk range of this batch (hub rows are processed in batches
   i64 f0, f1;             //   bounding the pool); fin-item range of the same rows
   i64 h0, h1;             // hub range of the batch
@@ -1222,7 +1223,6 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
   for (int s = threadIdx.x; s < CAPS; s += HUB_ACC_T) { skeys[s] = EMPTY; svals[s] = 0; }
   if (threadIdx.x == 0) scnt = 0;
   __syncthreads();
-  VT *pv = (VT *)hb.pval;
   for (i64 ci = hb.c0 + blockIdx.x; ci < hb.c1; ci += gridDim.x) {
     const Chunk ch = a.chunks[ci];
     const int32_t r = a.rows[ch.h];
@@ -1248,9 +1248,8 @@ __global__ void __launch_bounds__(HUB_ACC_T) k_hub_acc(AggArgs a, HubArgs hb) {
       const int sl = slist[t];
       const int32_t k = skeys[sl];
       const int pos = atomicAdd(&hist[hbucket(k, blg)], 1);
-      hb.pkey[base + pos] = k;
-      pv[base + pos] = svals[sl];
-      if (DEGL) hb.pdeg[base + pos] = sdeg[t];
+      const u64 val = (u64)svals[sl];
+      hb.pent[base + pos] = make_uint4((uint32_t)k, DEGL ? sdeg[t] : 0u, (uint32_t)val, (uint32_t)(val >> 32));
       skeys[sl] = EMPTY;
       svals[sl] = 0;
     }
@@ -1346,8 +1345,9 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
         const i64 base = (c - hb.c0) * HUB_CHUNK;
         for (int i = s0 + gl; i < s1; i += Gc) {
           const i64 e = base + i;
-          const int32_t k = hb.pkey[e];
-          const u64 v = (u64)((const VT *)hb.pval)[e];
+          const uint4 pe = hb.pent[e];
+          const int32_t k = (int32_t)pe.x;
+          const u64 v = (u64)pe.z | ((u64)pe.w << 32);
           if (*(volatile int *)&scnt >= MAXD - 1) { sovf = 1; continue; }
           bool claimed = false;
           const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
@@ -1355,7 +1355,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin(AggArgs a, HubArgs hb) {
             const int q = (int)atom_add_s32(cb, 1);
             if (q < MAXD) {
               slist[q] = (uint16_t)sl;
-              if (DEGL) sdeg[q] = hb.pdeg[e];
+              if (DEGL) sdeg[q] = pe.y;
             } else {
               sovf = 1;
             }
@@ -1474,8 +1474,9 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin_sw(AggArgs a, HubArgs hb)
         const i64 base = (c - hb.c0) * HUB_CHUNK;
         for (int i = s0 + gl; i < s1; i += Gc) {
           const i64 e = base + i;
-          const int32_t k = hb.pkey[e];
-          const u64 v = (u64)((const VT *)hb.pval)[e];
+          const uint4 pe = hb.pent[e];
+          const int32_t k = (int32_t)pe.x;
+          const u64 v = (u64)pe.z | ((u64)pe.w << 32);
           if (*(volatile int *)&scnt[par] >= MAXD - 1) { sovf[par] = 1; continue; }
           bool claimed = false;
           const unsigned sl = tab_insert<VT>(kb, vb, CAPF - 1, FLG, k, v, &claimed);
@@ -1483,7 +1484,7 @@ __global__ void __launch_bounds__(HUB_FIN_T) k_hub_fin_sw(AggArgs a, HubArgs hb)
             const int q = (int)atom_add_s32(cb, 1);
             if (q < MAXD) {
               slist[q] = (uint16_t)sl;
-              sdeg[q] = hb.pdeg[e];
+              sdeg[q] = pe.y;
             } else {
               sovf[par] = 1;
             }

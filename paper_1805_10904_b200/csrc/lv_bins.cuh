@@ -86,9 +86,9 @@ struct Bins {
   int fin_lg = HUB_FIN_LG;
   Buf<Chunk> chunks;
   Buf<i64> cfirst, bfirst, segoff;
-  Buf<int32_t> ccount, blg, seg, pkey;
-  Buf<u64> pval, emit_cur;                 // pval holds uint32 or u64 values (VT)
-  Buf<uint32_t> pdeg;                      // pool: deg_C of each entry (SWEEP/MERGE)
+  Buf<int32_t> ccount, blg, seg;
+  Buf<u64> emit_cur;
+  Buf<uint4> pent;                         // pool: {key, deg_C, Σw lo, Σw hi} per entry
   std::vector<i64> batch_h;                // hub-row batches: [batch_h[i], batch_h[i+1])
   std::vector<i64> h_cfirst, h_bfirst;     // host copies (chunk / fin-item starts, + end)
   i64 pool_chunks = 0;                     // pool capacity in chunks (max over batches)
@@ -424,9 +424,7 @@ inline void finish_bins(Ctx &c, const i64 *ptr, i64 universe, Bins &B, const std
     B.batch_h.push_back(B.nhub);
     for (size_t i = 0; i + 1 < B.batch_h.size(); ++i)
       B.pool_chunks = std::max(B.pool_chunks, B.h_cfirst[B.batch_h[i + 1]] - B.h_cfirst[B.batch_h[i]]);
-    B.pkey.alloc(c.A, B.pool_chunks * HUB_CHUNK);
-    B.pval.alloc(c.A, B.pool_chunks * HUB_CHUNK);  // sized for u64; uint32 uses half
-    B.pdeg.alloc(c.A, B.pool_chunks * HUB_CHUNK);
+    B.pent.alloc(c.A, B.pool_chunks * HUB_CHUNK);  // packed 16-byte pool entries
     B.fitem.alloc(c.A, B.nfin);
     B.part.alloc(c.A, B.nfin);
     B.emit_cur.alloc(c.A, B.nhub);
@@ -568,9 +566,7 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
     hb.bfirst = B.bfirst.p;
     hb.segoff = B.segoff.p;
     hb.seg = B.seg.p;
-    hb.pkey = B.pkey.p;
-    hb.pval = (void *)B.pval.p;
-    hb.pdeg = B.pdeg.p;
+    hb.pent = B.pent.p;
     hb.fitem = B.fitem.p;
     hb.part = B.part.p;
     hb.emit_cur = B.emit_cur.p;
