@@ -621,13 +621,26 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
     if (tab) {
       // warps per row: measured r2 (C4 level 0; 16 -> 32 warps: 1.24 -> 1.11 ms, 2 -> 4:
       // 1.24 -> 1.02 ms, 8 -> 16 in the 4096 bin: 1.45 -> 1.49 ms)
-      if (B.count(10)) { set(10); launch_tab<32, 16384, WT>(c, tm, a, nm(10).c_str(), st(1), s64all); }
-      if (B.count(9)) { set(9); launch_tab<8, 8192, WT>(c, tm, a, nm(9).c_str(), st(0), s64all); }
-      if (B.count(8)) { set(8); launch_tab<4, 4096, WT>(c, tm, a, nm(8).c_str(), st(1), s64all); }
-      if (B.count(7)) { set(7); launch_tab<4, 2048, WT>(c, tm, a, nm(7).c_str(), st(2), s64all); }
-      if (B.count(6)) { set(6); launch_tab<1, 1024, WT>(c, tm, a, nm(6).c_str(), st(0), s64all); }
-      if (B.count(5)) { set(5); launch_tab<1, 512, WT>(c, tm, a, nm(5).c_str(), st(1), s64all); }
-      if (B.count(4)) { set(4); launch_tab<1, 256, WT>(c, tm, a, nm(4).c_str(), st(2), s64all); }
+      // edges per lane per batch: 2 in the 129-256, 513-1024, 2049-4096 and 4097-8192 bins
+      // (C4 level 0: 0.76 -> 0.71, 1.02 -> 0.95, 1.39 -> 1.30, 1.03 -> 0.96 ms — the smaller
+      // batches keep fewer registers live and fill their last batch better), 4 elsewhere
+      // (the 1025-2048 bin: 0.59 -> 0.65 ms with 2).
+      // LV_TAB_U2 (experiments): bit b = bin b with 2 edges per lane.
+      static const int u2 = getenv("LV_TAB_U2") ? atoi(getenv("LV_TAB_U2")) : (32 | 128 | 512 | 1024);
+#define LV_TABU(b, W_, C_, S_)                                                                \
+  if (B.count(b)) {                                                                          \
+    set(b);                                                                                  \
+    if ((u2 >> (b)) & 1) launch_tab<W_, C_, WT, 2>(c, tm, a, nm(b).c_str(), st(S_), s64all); \
+    else launch_tab<W_, C_, WT>(c, tm, a, nm(b).c_str(), st(S_), s64all);                    \
+  }
+      LV_TABU(10, 32, 16384, 1)
+      LV_TABU(9, 8, 8192, 0)
+      LV_TABU(8, 4, 4096, 1)
+      LV_TABU(7, 4, 2048, 2)
+      LV_TABU(6, 1, 1024, 0)
+      LV_TABU(5, 1, 512, 1)
+      LV_TABU(4, 1, 256, 2)
+#undef LV_TABU
     }
   }
   if (!tab) {
