@@ -621,16 +621,19 @@ void launch_agg(Ctx &c, const Bins &B, AggArgs a, KTimer *tm = nullptr, bool s64
     if (tab) {
       // warps per row: measured r2 (C4 level 0; 16 -> 32 warps: 1.24 -> 1.11 ms, 2 -> 4:
       // 1.24 -> 1.02 ms, 8 -> 16 in the 4096 bin: 1.45 -> 1.49 ms)
-      // edges per lane per batch: 2 in the 129-256, 513-1024, 2049-4096 and 4097-8192 bins
-      // (C4 level 0: 0.76 -> 0.71, 1.02 -> 0.95, 1.39 -> 1.30, 1.03 -> 0.96 ms — the smaller
-      // batches keep fewer registers live and fill their last batch better), 4 elsewhere
-      // (the 1025-2048 bin: 0.59 -> 0.65 ms with 2).
-      // LV_TAB_U2 (experiments): bit b = bin b with 2 edges per lane.
-      static const int u2 = getenv("LV_TAB_U2") ? atoi(getenv("LV_TAB_U2")) : (32 | 128 | 512 | 1024);
+      // edges per lane per batch (C4 level 0, CUDA events, profiles/r2a[tuvw]_sweep_variants.txt):
+      // 1 in the 4097-8192 bin (1.03 -> 0.84 ms) and the 33-128 bin (0.70 -> 0.68 ms); 2 in the
+      // 129-256, 513-1024 and 2049-4096 bins (0.76 -> 0.71, 1.02 -> 0.95, 1.39 -> 1.30 ms) — the
+      // smaller batches keep fewer registers live and fill a row's last batch better; 4 in the
+      // 1025-2048 bin (0.59 -> 0.65 ms with 2, 0.84 with 1 at level 1).
+      // LV_TAB_U1 / LV_TAB_U2 (experiments): bit b = bin b with 1 / 2 edges per lane.
+      static const int u2 = getenv("LV_TAB_U2") ? atoi(getenv("LV_TAB_U2")) : (32 | 128 | 512);
+      static const int u1 = getenv("LV_TAB_U1") ? atoi(getenv("LV_TAB_U1")) : (16 | 1024);
 #define LV_TABU(b, W_, C_, S_)                                                                \
   if (B.count(b)) {                                                                          \
     set(b);                                                                                  \
-    if ((u2 >> (b)) & 1) launch_tab<W_, C_, WT, 2>(c, tm, a, nm(b).c_str(), st(S_), s64all); \
+    if ((u1 >> (b)) & 1) launch_tab<W_, C_, WT, 1>(c, tm, a, nm(b).c_str(), st(S_), s64all); \
+    else if ((u2 >> (b)) & 1) launch_tab<W_, C_, WT, 2>(c, tm, a, nm(b).c_str(), st(S_), s64all); \
     else launch_tab<W_, C_, WT>(c, tm, a, nm(b).c_str(), st(S_), s64all);                    \
   }
       LV_TABU(10, 32, 16384, 1)
