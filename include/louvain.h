@@ -92,7 +92,14 @@ typedef struct {
     louvain_alloc_fn alloc;  /* optional allocator hook (see above)                     */
     louvain_free_fn free;
     void *alloc_ctx;
-    void *nccl_comm;         /* ncclComm_t for the sweep-sharded path; NULL = 1 GPU     */
+    void *nccl_comm;         /* ncclComm_t for the sweep-sharded path; NULL = 1 GPU.
+                                Every rank then holds the whole (replicated) level graph
+                                and state, sweeps its edge-balanced vertex range, and
+                                computes its row part of the CSR build and of each
+                                contraction; louvain_create and louvain_run are
+                                COLLECTIVE over the communicator (every rank calls them with
+                                the same graph and configuration, on its own device).  Results
+                                equal the 1-GPU run.                                      */
     int32_t rank, world;     /* this process's rank / world size in nccl_comm           */
     int32_t profile;         /* 1: time every sweep kernel with CUDA events during run   */
     int32_t coloring;        /* SURVEY F2, reading D29 (Lu et al.'s colouring heuristic,
