@@ -41,7 +41,7 @@ def _canon(rp, col, w):
     return col[o], w[o]
 
 
-def _stepwise(name, check, sweeps, threads=None):
+def _stepwise(name, check, sweeps, threads=None, compare_contraction=True):
     import torch
 
     psutil = pytest.importorskip("psutil")
@@ -87,6 +87,7 @@ def _stepwise(name, check, sweeps, threads=None):
         qs = [lv.modularity(l) for l in range(L)]
         final = lv.partition(-1)
         g = og
+        del og  # (C5: the level graphs are dropped as soon as the next one is built)
         for l in range(L):
             p = parts[l]
             assert len(p) == g.n
@@ -96,7 +97,7 @@ def _stepwise(name, check, sweeps, threads=None):
             assert m["Q"] == qs[l], (name, l, m["Q"], qs[l])
             if l + 1 < L:
                 h = g.induce(p, k)
-                if l == 0:
+                if l == 0 and compare_contraction:
                     a = lv.contract(p, k)
                     b = h.arrays()
                     assert np.array_equal(a["row_ptr"], b["row_ptr"])
@@ -121,7 +122,11 @@ def test_c5_rmat27_stepwise_equals_oracle():
     compared with the oracle's golden in test_gpu_fullsize_golden.py."""
     if os.environ.get("LV_STEPWISE_C5") != "1":
         pytest.skip("opt-in: LV_STEPWISE_C5=1 (C5 is covered by the golden full-run test)")
-    rep = _stepwise("rmat27", check={1, 2, 3, 4, 25, 50, 100}, sweeps=100)
+    # the level-0 contraction's CSR is compared at C4 only: its host copies and the
+    # canonicalising sort on top of the oracle's 51 GB CSR exceeded the box's 196 GB
+    # (r2be: killed after 760 s); at C5 the levels' exact Q on the oracle's own induced
+    # graphs covers the contraction
+    rep = _stepwise("rmat27", check={1, 2, 3, 4, 25, 50, 100}, sweeps=100, compare_contraction=False)
     print(rep)
 
 
